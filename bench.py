@@ -1,0 +1,313 @@
+"""Benchmark: exact QFT on 27 qubits (BASELINE.json configs[1]) on B200.
+
+Metric (BASELINE.json "QFT sec & HBM GB/s"): QFT gate-layers per second
+(one layer = H(j) plus its controlled-phase fan), whole job over all ranks;
+the line also carries the QFT seconds and the HBM GB/s of the fused sweeps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step is one full QFT-27 (fp32 amplitudes, 1 GiB, random normalised input,
+SWAPs as label permutations like the reference engine) on a resident state.
+`e2e` repeats it through the public C-ABI entry points with host buffers:
+pinned host state -> device, QFT, device -> host, copies inside the timing.
+`--impl reference` times the reference's CPU path (the oracle port of its
+NumPy kernels, oracle/ket_oracle.py) on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+N_QUBITS = 27
+CPP_CORES = 1  # the reference's NumPy ufuncs are single-threaded
+
+
+def qft_layers(n: int) -> int:
+    return n
+
+
+# ---------------------------------------------------------------------------
+# CPU reference path (oracle port of the reference's kernels)
+# ---------------------------------------------------------------------------
+def cpu_layer_sample(n: int, n_cp: int | None = None):
+    """Time one 'average' QFT layer of the reference's dense loop at width n:
+    one H plus (n-1)/2 controlled phases (QFT-n = n H + C(n,2) CP), complex128,
+    through the oracle's kernel-identical NumPy expressions (ket.py:133-164)."""
+    import numpy as np
+
+    from oracle import ket_oracle as O
+    from paper_2304_14969_b200.circuit import gate_matrix
+
+    n_cp = (n - 1) // 2 if n_cp is None else n_cp
+    amps = np.zeros(1 << n, dtype=complex)
+    amps[0] = amps[-1] = 2 ** -0.5
+    H = gate_matrix("h")
+    j = n - 1
+    t0 = time.perf_counter()
+    O.apply_1q(amps, j, H)
+    t1 = time.perf_counter()
+    for k in range(1, n_cp + 1):
+        O.apply_controlled(amps, (j - k,), (1,), j, gate_matrix("p", (math.pi / (1 << k),)))
+    t2 = time.perf_counter()
+    return t1 - t0, (t2 - t1) / max(1, n_cp)
+
+
+def cpu_baseline(n: int):
+    t_h, t_cp = cpu_layer_sample(n, 4)
+    t_qft = n * t_h + (n * (n - 1) // 2) * t_cp
+    return {"value": qft_layers(n) / t_qft, "unit": "gate-layers/s", "cores": CPP_CORES, "kind": "port",
+            "qft_sec": t_qft,
+            "sample": f"1 H + 4 CP kernels of QFT-{n} on a 2^{n} complex128 state via the oracle port of the "
+                      f"reference's NumPy kernels (ket.py:133-164), 1 thread; extrapolated to the QFT-{n} mix "
+                      f"of {n} H + {n * (n - 1) // 2} CP (SWAPs as label swaps, engine.py:525-535)"}
+
+
+def run_reference(args, rank: int, world: int):
+    if rank != 0:
+        return
+    n = args.qubits
+    times = []
+    for i in range(args.warmup + args.steps):
+        t_h, t_cp = cpu_layer_sample(n)
+        if i >= args.warmup:
+            times.append(t_h + ((n - 1) // 2) * t_cp)
+    t = statistics.mean(times)
+    value = 1.0 / t
+    line = {"metric": f"QFT-{n} gate-layers/s", "value": value, "unit": "gate-layers/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": f"exact QFT on {n} qubits (BASELINE configs[1]); reference CPU path",
+                       "qubits": n, "step": f"one average QFT-{n} layer: 1 H + {(n - 1) // 2} CP kernels"},
+            "qft_sec": n * t,
+            "cpu_baseline": {"value": value, "unit": "gate-layers/s", "cores": CPP_CORES, "kind": "port",
+                             "sample": f"each step = 1 H + {(n - 1) // 2} CP kernels at width {n}, complex128, "
+                                       f"oracle port of ket.py:133-164 (NumPy, single-threaded)"},
+            "e2e": {"value": value, "unit": "gate-layers/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (NVML, in-process) for the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x1: "gpu_idle"}
+
+    def __init__(self, device: int):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self.nv is not None:
+            self.t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args, rank: int, world: int):
+    import numpy as np
+    import torch
+
+    from paper_2304_14969_b200 import _lib
+    from paper_2304_14969_b200.circuit import build_qft
+    from paper_2304_14969_b200.executor import compile_circuit
+    from paper_2304_14969_b200.ket import DenseKet, set_default_device
+
+    dev = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(dev)
+    set_default_device(dev)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    stream = torch.cuda.current_stream()
+    _lib.call("sk_set_stream", dev, stream.cuda_stream)
+
+    n, dtype = args.qubits, args.dtype
+    prog = compile_circuit(build_qft(n), dtype=dtype, device=dev)
+    nsw = prog.n_sweeps
+    elem = 8 if dtype == "c64" else 16
+    state_bytes = (1 << n) * elem
+
+    # random normalised input generated on the device (not timed)
+    g = torch.Generator(device=f"cuda:{dev}").manual_seed(1234 + rank)
+    st = DenseKet(n, dtype=dtype, device=dev)
+    real = torch.float32 if dtype == "c64" else torch.float64
+    x = torch.randn(2 << n, device=f"cuda:{dev}", dtype=real, generator=g)
+    x /= torch.linalg.vector_norm(x)
+    _lib.call("sk_copy_from_device", st._h, x.data_ptr(), 1 << n)  # torch is plumbing only
+    torch.cuda.synchronize()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        prog.run(st)
+    barrier()
+
+    # timed region: K QFTs, events between sweeps for per-launch durations
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nsw + 1)] for _ in range(args.steps)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clk:
+        barrier()
+        start.record(stream)
+        for k in range(args.steps):
+            evs[k][0].record(stream)
+            for s_ in range(nsw):
+                prog.run(st, s_, 1)
+                evs[k][s_ + 1].record(stream)
+        stop.record(stream)
+        torch.cuda.synchronize()
+        # keep the sampler alive a little so short regions still get samples
+        if len(clk.samples) < 20:
+            t_end = time.time() + 0.2
+            while time.time() < t_end:
+                prog.run(st)
+            torch.cuda.synchronize()
+    ms = start.elapsed_time(stop)
+    launch_ms = [evs[k][i].elapsed_time(evs[k][i + 1]) for k in range(args.steps) for i in range(nsw)]
+    if dist is not None:
+        t = torch.tensor([ms], device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = world * qft_layers(n) / (ms_per_step / 1e3)
+    avg_launch = statistics.mean(launch_ms)
+    per_launch_bytes = prog.bytes_per_sweep()
+    achieved_gbs = per_launch_bytes / (avg_launch / 1e3) / 1e9
+
+    # ---- e2e through the public API with host buffers --------------------
+    host = torch.empty(2 << n, dtype=real, pin_memory=True)
+    host.copy_(x)
+    del x
+    out_host = torch.empty_like(host)
+    for _ in range(2):
+        _lib.call("sk_upload_native", st._h, host.data_ptr(), 1 << n)
+        prog.run(st)
+        _lib.call("sk_download_native", st._h, out_host.data_ptr(), 1 << n)
+    e2e_steps = max(3, min(args.steps, 10))
+    barrier()
+    t0 = time.perf_counter()
+    e_start, e_stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e_start.record(stream)
+    for _ in range(e2e_steps):
+        _lib.call("sk_upload_native", st._h, host.data_ptr(), 1 << n)
+        prog.run(st)
+        _lib.call("sk_download_native", st._h, out_host.data_ptr(), 1 << n)
+    e_stop.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e_start.elapsed_time(e_stop) / e2e_steps
+    if dist is not None:
+        t = torch.tensor([e2e_ms], device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    peak = peaks.get("hbm_gbs", 6650.0)
+    traffic = None
+    prof = ROOT / "profiles" / "ncu_summary.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get("dram_bytes_per_sweep")
+        except Exception:
+            traffic = None
+
+    if rank == 0:
+        cpu = cpu_baseline(n) if (world == 1 and not args.no_cpu) else None
+        line = {
+            "metric": f"QFT-{n} gate-layers/s", "value": value, "unit": "gate-layers/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+            "config": {"workload": f"exact QFT on {n} qubits, 1xB200 per rank (BASELINE configs[1])",
+                       "qubits": n, "state_bytes": state_bytes, "input": "random normalised state, device-generated",
+                       "l2": "state (1 GiB) > L2 (126 MB): no flush needed", "swaps": "label permutations",
+                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+            "qft_sec": ms_per_step / 1e3,
+            "hbm_gbs": nsw * per_launch_bytes / (ms_per_step / 1e3) / 1e9,
+            "sweeps_per_qft": nsw,
+            "unfused_bytes_per_qft": 2 * elem * (n * (1 << n) + (n * (n - 1) // 2) * (1 << (n - 1))),
+            "gpu_launches": args.steps * nsw,
+            "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
+                         "frac": achieved_gbs / peak, "traffic": traffic,
+                         "kernel": "k_sweep<float,4>" if dtype == "c64" else "k_sweep<double,3>",
+                         "algorithmic_bytes_per_launch": per_launch_bytes, "avg_launch_ms": avg_launch,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
+            "clocks": clk.summary(),
+            "e2e": {"value": world * qft_layers(n) / (e2e_ms / 1e3), "unit": "gate-layers/s",
+                    "h2d_bytes_per_step": state_bytes, "d2h_bytes_per_step": state_bytes,
+                    "ms_per_step": e2e_ms, "path": "sk_upload_native + sk_program_run + sk_download_native"},
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--qubits", type=int, default=N_QUBITS)
+    ap.add_argument("--dtype", default="c64", choices=["c64", "c128"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", args.gpus if "RANK" in os.environ else 1))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,26 @@
+"""Exceptions shared by the ket engine and its callers.
+
+`MemoryBudgetError` mirrors the reference's recoverable budget error
+(engine.py:38-44): raised BEFORE any allocation, state left usable.
+"""
+from __future__ import annotations
+
+
+class MemoryBudgetError(RuntimeError):
+    """A merge/conversion/allocation would exceed the dense amplitude budget."""
+
+    def __init__(self, needed: int, budget: int, detail: str | None = None):
+        msg = f"needs {needed} dense amplitudes, budget is {budget}"
+        if detail:
+            msg += f" ({detail})"
+        super().__init__(msg)
+        self.needed = needed
+        self.budget = budget
+
+
+class InvariantError(RuntimeError):
+    """Internal consistency violation (a bug, not a user error); engine.py:47-48."""
+
+
+class DeviceError(RuntimeError):
+    """A CUDA runtime failure inside libshardcu."""

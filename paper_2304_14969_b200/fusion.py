@@ -1,0 +1,372 @@
+"""Gate-fusion planner for the fused dense executor.
+
+Turns a circuit into a program for `k_sweep` (csrc/sk_fused.cu): a list of
+sweeps, each one HBM read + write of the state, each holding stages of ops
+applied on register-resident amplitudes.  The reference's counterpart is the
+gate-by-gate loop `dense_reference` (validate.py:83-111), one NumPy pass per
+gate; SWAPs become label permutations as in the engine (engine.py:525-535).
+
+Lowering (per gate, on physical bits):
+  * 1q / controlled gate with an exactly diagonal matrix (the reference's
+    fast-path test, ket.py:136,153)          -> DIAG (needs no pairing)
+  * otherwise                                -> MAT on its target
+  * a run of consecutive diagonal ops is reordered freely (they commute);
+    controlled phases sharing a target whose controls form a contiguous bit
+    field with angles pi*s*2^(c-lo) collapse into ONE RAMP op
+    exp(i*pi*s*F), F = (idx >> lo) & (2^k - 1): the QFT's fan-in of CPs.
+
+Scheduling: op A may move ahead of op B iff neither acts non-diagonally on a
+bit the other touches.  A sweep greedily takes every op (in order) that
+commutes with all ops left behind and whose non-diagonal target fits the
+tile (T bits, always including the lowest `low_bits` bits so warps stream
+>= 256 contiguous bytes).  Inside a sweep, stages are packed the same way
+with capacity NR register bits; the first and last stage keep their
+register bits off the low bits so HBM loads and stores stay coalesced.
+"""
+from __future__ import annotations
+
+import cmath
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .circuit import Circuit, gate_matrix
+
+MAT, DIAG, RAMP = _lib.SK_OP_MAT, _lib.SK_OP_DIAG, _lib.SK_OP_RAMP
+MAX_STAGES = _lib.SK_MAX_STAGES
+
+# kernel geometry per dtype (csrc/sk_fused.cu): register bits, max tile bits,
+# low contiguous bits (256 B per warp access)
+GEOMETRY = {"c64": dict(nreg=4, tile=13, low=5), "c128": dict(nreg=3, tile=12, low=4)}
+
+
+@dataclass
+class Op:
+    kind: int
+    qubit: int
+    m: tuple  # 8 doubles
+    ctrl_mask: int = 0
+    ctrl_val: int = 0
+    nbits: int = 0
+    src: int = -1  # index of the originating gate (diagnostics)
+
+    @property
+    def tmask(self) -> int:
+        """Bits acted on non-diagonally."""
+        return (1 << self.qubit) if self.kind == MAT else 0
+
+    @property
+    def smask(self) -> int:
+        """Every bit the op reads or acts on."""
+        if self.kind == RAMP:
+            s = ((1 << self.nbits) - 1) << self.qubit
+        else:
+            s = 1 << self.qubit
+        return s | self.ctrl_mask
+
+
+def _m8(m) -> tuple:
+    return (m[0, 0].real, m[0, 0].imag, m[0, 1].real, m[0, 1].imag,
+            m[1, 0].real, m[1, 0].imag, m[1, 1].real, m[1, 1].imag)
+
+
+def lower(circuit: Circuit, phys: list[int] | None = None):
+    """Gates -> elementary ops on physical bits; returns (ops, phys) where
+    phys[label] is the physical bit holding logical qubit `label` at the end."""
+    n = circuit.width
+    phys = list(range(n)) if phys is None else list(phys)
+    ops: list[Op] = []
+    for gi, g in enumerate(circuit.gates):
+        if g.name == "m":
+            raise ValueError("measurement gates are not fusable; split the circuit at them")
+        if g.name == "swap":
+            a, b = g.targets
+            phys[a], phys[b] = phys[b], phys[a]
+            continue
+        m = gate_matrix(g.name, g.params)
+        t = phys[g.targets[0]]
+        cmask = cval = 0
+        for c, pol in zip(g.controls, g.polarity):
+            cmask |= 1 << phys[c]
+            if pol:
+                cval |= 1 << phys[c]
+        diag = m[0, 1] == 0 and m[1, 0] == 0
+        if diag and m[0, 0] == 1 and m[1, 1] == 1:
+            continue  # identity (ket.py:154-158 skips both entries)
+        ops.append(Op(DIAG if diag else MAT, t, _m8(m), cmask, cval, src=gi))
+    return ops, phys
+
+
+def _wrap(a: float) -> float:
+    return (a + math.pi) % (2 * math.pi) - math.pi
+
+
+def _try_ramp(target: int, group: list[Op]) -> Op | None:
+    """Collapse controlled phases diag(1, e^{i phi_c}) on `target` with single
+    controls c (polarity 1) into one RAMP if the controls are a contiguous
+    field and phi_c = pi * s * 2^(c - lo)."""
+    if len(group) < 2:
+        return None
+    phis = {}
+    for op in group:
+        if op.ctrl_mask == 0 or op.ctrl_mask & (op.ctrl_mask - 1) or op.ctrl_val != op.ctrl_mask:
+            return None
+        if op.m[0] != 1.0 or op.m[1] != 0.0:
+            return None
+        c = op.ctrl_mask.bit_length() - 1
+        if c in phis:
+            return None
+        phis[c] = math.atan2(op.m[7], op.m[6])
+    lo, hi = min(phis), max(phis)
+    if hi - lo + 1 != len(phis):
+        return None
+    s = phis[lo] / math.pi
+    for c, phi in phis.items():
+        if abs(_wrap(phi - math.pi * s * (1 << (c - lo)))) > 1e-12:
+            return None
+    return Op(RAMP, lo, (s, 0, 0, 0, 0, 0, 0, 0), 1 << target, 1 << target, nbits=hi - lo + 1,
+              src=group[0].src)
+
+
+def fuse_diagonal_runs(ops: list[Op]) -> list[Op]:
+    """Within each maximal run of consecutive diagonal ops, collapse QFT-style
+    controlled-phase fans into RAMP ops (diagonal ops commute, so the run may
+    be regrouped by target)."""
+    out: list[Op] = []
+    i = 0
+    while i < len(ops):
+        if ops[i].kind != DIAG:
+            out.append(ops[i])
+            i += 1
+            continue
+        j = i
+        while j < len(ops) and ops[j].kind == DIAG:
+            j += 1
+        run = ops[i:j]
+        by_target: dict[int, list[Op]] = {}
+        order: list[int] = []
+        for op in run:
+            if op.qubit not in by_target:
+                by_target[op.qubit] = []
+                order.append(op.qubit)
+            by_target[op.qubit].append(op)
+        for t in order:
+            grp = by_target[t]
+            ramp = _try_ramp(t, grp)
+            out.extend([ramp] if ramp is not None else grp)
+        i = j
+    return out
+
+
+def _pack(ops: list[Op], capacity: int, base_mask: int):
+    """Greedy commutation-aware packing: take every op that commutes with all
+    skipped ops and whose non-diagonal target fits `capacity` bits together
+    with `base_mask`.  Returns (taken, skipped, mask)."""
+    mask = base_mask
+    taken, skipped = [], []
+    sk_t = sk_s = 0
+    for op in ops:
+        t, s = op.tmask, op.smask
+        if (t & sk_s) == 0 and (sk_t & s) == 0 and bin(mask | t).count("1") <= capacity:
+            taken.append(op)
+            mask |= t
+        else:
+            skipped.append(op)
+            sk_t |= t
+            sk_s |= s
+    return taken, skipped, mask
+
+
+@dataclass
+class StagePlan:
+    reg_bits: list[int]
+    ops: list[Op] = field(default_factory=list)
+
+
+@dataclass
+class SweepPlan:
+    tile_bits: list[int]
+    stages: list[StagePlan]
+
+
+@dataclass
+class Plan:
+    width: int
+    dtype: str
+    nreg: int
+    sweeps: list[SweepPlan]
+    phys: list[int]
+    n_gates: int
+    n_ops: int
+
+    @property
+    def order(self) -> list[int]:
+        """`permute_qubits` order taking the physical result to label order."""
+        return list(self.phys)
+
+
+def _bits(mask: int) -> list[int]:
+    out = []
+    b = 0
+    while mask:
+        if mask & 1:
+            out.append(b)
+        mask >>= 1
+        b += 1
+    return out
+
+
+def _stages_for(ops: list[Op], tile: list[int], nreg: int, low: int) -> list[StagePlan]:
+    """Split a sweep's ops into register stages (commutation-aware greedy) and
+    pad every stage to exactly nreg register bits."""
+    stages: list[StagePlan] = []
+    rest = list(ops)
+    while rest:
+        taken, rest, mask = _pack(rest, nreg, 0)
+        stages.append(StagePlan(_bits(mask), taken))
+    if not stages:
+        stages.append(StagePlan([], []))
+    low_mask = (1 << low) - 1
+    tile_desc = sorted(tile, reverse=True)
+
+    def pad(regs: list[int], avoid_low: bool) -> list[int]:
+        regs = list(regs)
+        for b in tile_desc:
+            if len(regs) >= nreg:
+                break
+            if b not in regs and not (avoid_low and (1 << b) & low_mask):
+                regs.append(b)
+        for b in tile_desc:  # tiny tiles: fall back to any bit
+            if len(regs) >= nreg:
+                break
+            if b not in regs:
+                regs.append(b)
+        return regs
+
+    coalesce = len(tile) - nreg >= low  # enough thread bits to keep lanes on the low bits
+    first_bad = coalesce and any((1 << b) & low_mask for b in stages[0].reg_bits)
+    if first_bad:
+        stages.insert(0, StagePlan([], []))
+    last_bad = coalesce and any((1 << b) & low_mask for b in stages[-1].reg_bits)
+    if last_bad:
+        stages.append(StagePlan([], []))
+    for i, st in enumerate(stages):
+        edge = i == 0 or i == len(stages) - 1
+        st.reg_bits = pad(st.reg_bits, avoid_low=edge and coalesce)
+    return stages
+
+
+def plan_ops(ops: list[Op], width: int, dtype: str = "c64", tile_bits: int | None = None,
+             low_bits: int | None = None, phys=None, n_gates: int = 0) -> Plan:
+    geo = GEOMETRY[dtype]
+    nreg = geo["nreg"]
+    T = min(tile_bits or geo["tile"], width)
+    low = min(low_bits if low_bits is not None else geo["low"], T)
+    if T < nreg:
+        raise ValueError(f"width {width} too small for the fused kernel (needs >= {nreg})")
+    base = (1 << low) - 1
+    sweeps: list[SweepPlan] = []
+    remaining = list(ops)
+    while remaining:
+        taken, skipped, mask = _pack(remaining, T, base)
+        # fill the tile with the lowest unused bits (more coalescing, same cost)
+        b = 0
+        while bin(mask).count("1") < T:
+            mask |= 1 << b
+            b += 1
+        tile = _bits(mask)
+        stages = _stages_for(taken, tile, nreg, low)
+        if len(stages) > MAX_STAGES:
+            # keep the ops of the first stages only; the rest go back in order
+            keep = []
+            while True:
+                st = _stages_for(taken[: len(keep) + 1], tile, nreg, low)
+                if len(st) > MAX_STAGES:
+                    break
+                keep = taken[: len(keep) + 1]
+            executed = {id(o) for o in keep}
+            stages = _stages_for(keep, tile, nreg, low)
+            remaining = [o for o in remaining if id(o) not in executed]
+        else:
+            remaining = skipped
+        sweeps.append(SweepPlan(tile, stages))
+    return Plan(width, dtype, nreg, sweeps, list(phys) if phys is not None else list(range(width)),
+                n_gates, len(ops))
+
+
+def plan_circuit(circuit: Circuit, dtype: str = "c64", tile_bits: int | None = None,
+                 low_bits: int | None = None, fuse: bool = True) -> Plan:
+    ops, phys = lower(circuit)
+    if fuse:
+        ops = fuse_diagonal_runs(ops)
+    return plan_ops(ops, circuit.width, dtype, tile_bits, low_bits, phys, len(circuit.gates))
+
+
+def to_c(plan: Plan):
+    """Plan -> (SkSweep array, SkOp array) for sk_program_create."""
+    flat: list[Op] = []
+    sweeps = (_lib.SkSweep * len(plan.sweeps))()
+    for si, sp in enumerate(plan.sweeps):
+        cs = sweeps[si]
+        cs.ntile = len(sp.tile_bits)
+        for i, b in enumerate(sp.tile_bits):
+            cs.tile_bits[i] = b
+        cs.nstages = len(sp.stages)
+        for s, st in enumerate(sp.stages):
+            for p, b in enumerate(st.reg_bits):
+                cs.reg_bits[s][p] = b
+            cs.op_begin[s] = len(flat)
+            flat.extend(st.ops)
+        cs.op_begin[len(sp.stages)] = len(flat)
+    ops = (_lib.SkOp * max(1, len(flat)))()
+    for i, op in enumerate(flat):
+        co = ops[i]
+        co.kind = op.kind
+        co.qubit = op.qubit
+        co.nbits = op.nbits
+        co.ctrl_mask = op.ctrl_mask
+        co.ctrl_val = op.ctrl_val
+        for k in range(8):
+            co.m[k] = float(op.m[k])
+    return sweeps, ops, len(flat)
+
+
+# ---------------------------------------------------------------------------
+# host-side interpreter of a plan's op semantics (used by the CPU tests to
+# check lowering, RAMP fusion and commutation-based reordering; the device
+# kernel is checked against the oracle on the GPU)
+# ---------------------------------------------------------------------------
+def apply_op_numpy(amps: np.ndarray, op: Op) -> None:
+    n = amps.size
+    idx = np.arange(n, dtype=np.int64)
+    sel = (idx & op.ctrl_mask) == op.ctrl_val
+    if op.kind == MAT:
+        bit = 1 << op.qubit
+        i0 = idx[sel & ((idx & bit) == 0)]
+        i1 = i0 | bit
+        m = op.m
+        m00, m01, m10, m11 = complex(m[0], m[1]), complex(m[2], m[3]), complex(m[4], m[5]), complex(m[6], m[7])
+        a0, a1 = amps[i0].copy(), amps[i1].copy()
+        amps[i0] = m00 * a0 + m01 * a1
+        amps[i1] = m10 * a0 + m11 * a1
+    elif op.kind == DIAG:
+        m = op.m
+        d = np.where((idx >> op.qubit) & 1, complex(m[6], m[7]), complex(m[0], m[1]))
+        amps[sel] *= d[sel]
+    else:
+        f = (idx >> op.qubit) & ((1 << op.nbits) - 1)
+        x = np.mod(op.m[0] * f.astype(np.float64), 2.0)
+        amps[sel] *= np.exp(1j * np.pi * x[sel])
+
+
+def run_plan_numpy(plan: Plan, amps: np.ndarray) -> np.ndarray:
+    for sp in plan.sweeps:
+        for st in sp.stages:
+            for op in st.ops:
+                if op.kind == MAT:
+                    assert op.qubit in st.reg_bits and op.qubit in sp.tile_bits
+                apply_op_numpy(amps, op)
+    return amps
