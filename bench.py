@@ -164,7 +164,8 @@ def run_ours(args, rank: int, world: int):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream(device=dev)  # one stream: library kernels and the timing events
+    torch.cuda.set_stream(stream)
     _lib.call("sk_set_stream", dev, stream.cuda_stream)
 
     n, dtype = args.qubits, args.dtype

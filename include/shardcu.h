@@ -50,8 +50,10 @@ const char* sk_last_error(void);
 int sk_version(void);
 /* Number of visible CUDA devices (0 when none; never fails). */
 int sk_device_count(void);
-/* Use `stream` (a cudaStream_t cast to an integer; 0 = library default
- * stream) for every subsequent operation on `device`. */
+/* Use `stream` (a cudaStream_t cast to an integer; 0 = the legacy default
+ * stream, SK_OWN_STREAM = the library's own non-blocking stream, the
+ * initial setting) for every subsequent operation on `device`. */
+#define SK_OWN_STREAM UINT64_MAX
 int sk_set_stream(int device, uint64_t stream);
 int sk_get_stream(int device, uint64_t* stream);
 int sk_synchronize(int device);
@@ -180,6 +182,14 @@ int sk_program_reg_bits(int dtype, int* nreg);
 int sk_program_create(int width, int dtype, int device, const sk_sweep* sweeps, int nsweeps,
                       const sk_op* ops, int nops, sk_program** out);
 int sk_program_destroy(sk_program* p);
+/* Host-only introspection (no device needed): lower a program into the
+ * fused kernel's op list.  For each kernel op i: ints[12i..12i+11] =
+ * {kind, slot, pattern, element mask, flags, lo, nbits, tmask, tval, qmask,
+ * turn, field mask}, reals[24i..24i+23] = coefficients m[8] then twiddles tw[16].  stage_ops[(SK_MAX_STAGES+1)*s + t]
+ * = first kernel op of stage t of sweep s (the entry after the last stage
+ * holds the end).  Used by the CPU tests to emulate the kernel ops. */
+int sk_program_lower(int width, int dtype, const sk_sweep* sweeps, int nsweeps, const sk_op* ops, int nops,
+                     int64_t* ints, double* reals, int cap, int* count, int* stage_ops);
 /* Run sweeps [first, first+count) of the program on s (count < 0: all). */
 int sk_program_run(sk_state* s, const sk_program* p, int first, int count);
 int sk_program_nsweeps(const sk_program* p, int* n);

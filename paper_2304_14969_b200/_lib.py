@@ -79,6 +79,8 @@ _SIGS = {
     "sk_program_create": [C.c_int, C.c_int, C.c_int, C.POINTER(SkSweep), C.c_int, C.POINTER(SkOp), C.c_int,
                           C.POINTER(p_prog)],
     "sk_program_destroy": [p_prog],
+    "sk_program_lower": [C.c_int, C.c_int, C.POINTER(SkSweep), C.c_int, C.POINTER(SkOp), C.c_int,
+                         C.POINTER(C.c_int64), C.POINTER(C.c_double), C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)],
     "sk_program_run": [p_state, p_prog, C.c_int, C.c_int],
     "sk_program_nsweeps": [p_prog, C.POINTER(C.c_int)],
 }

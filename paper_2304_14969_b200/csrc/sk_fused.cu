@@ -10,209 +10,354 @@
 //
 // Inside a tile the sweep runs a sequence of stages.  In a stage each thread
 // holds 2^NR amplitudes in registers, spanning the stage's NR register bits,
-// and applies that stage's ops on them:
-//   MAT  — 2x2 on a register bit, predicated on arbitrary control bits
-//          (controls outside the tile are a per-tile predicate),
-//   DIAG — diag(d0, d1) on ANY qubit (diagonal gates need no pairing),
-//   RAMP — per-element phase exp(i*pi*s*F(idx)), F a bit field of the
-//          index: the fan-in of a run of controlled phases onto one target
-//          (the QFT's CP(pi/2^k) chain collapses to one RAMP per target).
-// Between stages the tile is exchanged through (XOR-swizzled) shared memory.
-// Stage 0 loads from HBM, the last stage stores back: one read and one
-// write of every amplitude per sweep.
+// and applies that stage's ops on them.  Between stages the tile is
+// exchanged through (XOR-swizzled) shared memory; stage 0 loads from HBM and
+// the last stage stores back: one read and one write per amplitude per sweep.
+// Element addresses are walked in Gray-code order, so each element costs one
+// 64-bit add (HBM) or one XOR (shared memory; the swizzle is GF(2)-linear).
+//
+// ABI ops (sk_op) are lowered per stage, on the host, into kernel ops whose
+// register-bit predicates are precomputed element masks:
+//   K_MAT    generic 2x2 on a register slot (K_MATR: real coefficients)
+//   K_BFLY   H-like 2x2: y0 = c0 (a0 + a1), y1 = c1 (a0 - a1), optionally
+//            with a per-thread phase tau folded into c1 (QFT's H(j)·RAMP(j))
+//   K_PHASE  a[e] *= c for e in the element mask, c = c1 if a thread-side
+//            bit is set else c0 (DIAG gates; RAMP's register part)
+//   K_TPHASE a[e] *= tau (RAMP's thread part)
+// tau = exp(2 pi i frac(F * turn / 2^64)), F a bit field of the thread's
+// index, `turn` the RAMP scale in 64-bit fixed-point turns: exact modular
+// arithmetic, then one MUFU sin/cos (fp32) or sincospi (fp64) per thread.
 #include <vector>
 
 #include "sk_internal.cuh"
 
 namespace sk {
 
-constexpr int kMaxT = SK_MAX_TILE_BITS;
 constexpr int kMaxS = SK_MAX_STAGES;
 constexpr int kMaxR = SK_MAX_REG_BITS;
+constexpr int kMaxRuns = 16;
+
+enum KKind : int { K_MAT = 0, K_MATR = 1, K_PHASE = 2, K_TPHASE = 3, K_BFLY = 4 };
+enum KFlag : unsigned { F_TPRED = 1, F_QMASK = 2, F_C0REAL = 4, F_FOLD = 8, F_TABLE = 16, F_C0ONE = 32 };
+
+struct Run {  // bits [src, src+w) of a counter go to bits [dst, dst+w)
+  uint8_t src, dst, w, pad;
+};
 
 struct DStage {
   int op_begin, op_end;
-  uint64_t thr_off[kMaxT];  // global index offset contributed by thread-index bit i
-  uint32_t thr_loc[kMaxT];  // tile-local offset of thread-index bit i
-  uint64_t reg_off[kMaxR];  // global offset of register slot p
-  uint32_t reg_loc[kMaxR];  // tile-local offset of register slot p
+  int ng, nl;
+  Run grun[kMaxRuns];       // thread index bits -> global index bits
+  Run lrun[kMaxRuns];       // thread index bits -> tile-local index bits
+  uint64_t reg_goff[kMaxR]; // byte offset of register slot p in HBM
+  uint32_t reg_soff[kMaxR]; // swizzled byte offset of register slot p in shared memory
 };
 
 struct DSweep {
   int ntile;
   int nstages;
-  int tile_bits[kMaxT];
+  int nb;
+  Run brun[kMaxRuns];  // tile index (blockIdx) bits -> non-tile global bits
   DStage st[kMaxS];
 };
 
-struct DOp {
-  int kind;
-  int slot;              // MAT: target slot; DIAG: qubit slot or -1
-  uint32_t rmask, rval;  // control predicate on register slots
-  uint64_t tmask, tval;  // control predicate on the thread-constant index part
-  uint64_t qmask;        // DIAG: qubit mask when not a register bit
-  int lo, nbits;         // RAMP field
-  double s;              // RAMP scale
-  double m[8];
-  double w[2 * kMaxR];   // RAMP: exp(i*pi*s*F(reg_off[p]))
+struct alignas(16) KHdr {
+  int16_t kind;
+  int8_t slot;
+  int8_t pat;
+  uint16_t emask;
+  uint8_t lo, nbits;
+  uint32_t flags;
+  uint32_t pad;
 };
 
-// swizzle of the tile-local index: fold the high bits into the low SB bits so
-// every stage's warp access pattern is bank-conflict free for contiguous
-// register-bit runs (SB = 4 for 8-byte, 3 for 16-byte elements)
+template <typename R>
+struct alignas(16) KOp {
+  KHdr h;
+  uint64_t tmask, tval;  // predicate on the thread-constant index part (F_TPRED)
+  uint64_t qmask;        // K_PHASE: c1 when (gthr & qmask) != 0 (F_QMASK)
+  uint64_t turn;         // phase scale in 2^-64 turns
+  uint64_t fmask;        // phase field mask (applied after >> lo)
+  uint64_t pad2;
+  R m[8];                // K_MAT: 2x2; K_PHASE: c0 = m[0..1], c1 = m[2..3]; K_BFLY: c0 = m[0..1], c1 = m[4..5]
+  R tw[16];              // K_BFLY (F_TABLE): extra row-1 twiddle per pair k (8 complex)
+};
+
+// swizzle of the tile-local index (element units): fold the high bits into
+// the low SB bits; linear over GF(2), so swz(a ^ b) = swz(a) ^ swz(b)
 template <int SB>
-__device__ __forceinline__ uint32_t swz(uint32_t l) {
+__host__ __device__ __forceinline__ uint32_t swz(uint32_t l) {
   uint32_t h = l >> SB;
   uint32_t f = h ^ (h >> SB) ^ (h >> (2 * SB)) ^ (h >> (3 * SB));
   return l ^ (f & ((1u << SB) - 1));
 }
 
-template <typename R>
-__device__ __forceinline__ void sincospi_r(double x, R* s, R* c);
-template <>
-__device__ __forceinline__ void sincospi_r<float>(double x, float* s, float* c) {
-  sincospif((float)x, s, c);
-}
-template <>
-__device__ __forceinline__ void sincospi_r<double>(double x, double* s, double* c) {
-  sincospi(x, s, c);
+__host__ __device__ constexpr int ctz_c(int k) {
+  int b = 0;
+  while (!((k >> b) & 1)) ++b;
+  return b;
 }
 
-template <typename R, int NR, int P>
-__device__ __forceinline__ void mat_slot(vec2_t<R> (&a)[1 << NR], const Mat2<R>& m, uint32_t rmask, uint32_t rval) {
-#pragma unroll
-  for (int e = 0; e < (1 << NR); ++e) {
-    if ((e >> P) & 1) continue;
-    if ((e & rmask) != rval) continue;
-    const int e1 = e | (1 << P);
-    vec2_t<R> y0 = cmad2<R>(m.m00, a[e], m.m01, a[e1]);
-    vec2_t<R> y1 = cmad2<R>(m.m10, a[e], m.m11, a[e1]);
-    a[e] = y0;
-    a[e1] = y1;
+__device__ __forceinline__ uint64_t deposit(uint64_t x, const Run* r, int n) {
+  uint64_t o = 0;
+  for (int i = 0; i < n; ++i) o |= ((x >> r[i].src) & ((1ull << r[i].w) - 1)) << r[i].dst;
+  return o;
+}
+
+template <typename R>
+__device__ __forceinline__ vec2_t<R> thread_phase(uint64_t turn, uint64_t gthr, int lo, uint64_t fmask) {
+  const uint64_t f = (gthr >> lo) & fmask;
+  const uint64_t t = f * turn;  // exact: frac(F * s / 2) in 2^-64 turns
+  if (sizeof(R) == 4) {
+    const float ang = (float)(int32_t)(uint32_t)(t >> 32) * 1.4629180792671596e-09f;  // 2 pi / 2^32, in [-pi, pi)
+    float fs, fc;
+    __sincosf(ang, &fs, &fc);
+    return mk<R>((R)fc, (R)fs);
+  } else {
+    const double x = (double)(int64_t)t * 1.0842021724855044e-19;  // 2 / 2^64: half-turns in [-1, 1)
+    double ds, dc;
+    sincospi(x, &ds, &dc);
+    return mk<R>((R)dc, (R)ds);
   }
 }
 
+template <int NR, int P>
+struct PairMask {
+  static constexpr uint32_t value() {
+    uint32_t f = 0;
+    for (int e = 0; e < (1 << NR); ++e)
+      if (!((e >> P) & 1)) f |= 1u << e;
+    return f;
+  }
+};
+
+template <typename R, int NR, int P>
+__device__ __forceinline__ void mat_slot(vec2_t<R> (&a)[1 << NR], const Mat2<R>& m, uint32_t emask) {
+  if (emask == PairMask<NR, P>::value()) {
+#pragma unroll
+    for (int e = 0; e < (1 << NR); ++e) {
+      if ((e >> P) & 1) continue;
+      const int e1 = e | (1 << P);
+      vec2_t<R> y0 = cmad2<R>(m.m00, a[e], m.m01, a[e1]);
+      vec2_t<R> y1 = cmad2<R>(m.m10, a[e], m.m11, a[e1]);
+      a[e] = y0;
+      a[e1] = y1;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < (1 << NR); ++e) {
+      if ((e >> P) & 1) continue;
+      if (!((emask >> e) & 1u)) continue;
+      const int e1 = e | (1 << P);
+      vec2_t<R> y0 = cmad2<R>(m.m00, a[e], m.m01, a[e1]);
+      vec2_t<R> y1 = cmad2<R>(m.m10, a[e], m.m11, a[e1]);
+      a[e] = y0;
+      a[e1] = y1;
+    }
+  }
+}
+
+template <typename R, int NR, int P>
+__device__ __forceinline__ void matr_slot(vec2_t<R> (&a)[1 << NR], R m00, R m01, R m10, R m11, uint32_t emask) {
+#pragma unroll
+  for (int e = 0; e < (1 << NR); ++e) {
+    if ((e >> P) & 1) continue;
+    if (!((emask >> e) & 1u)) continue;
+    const int e1 = e | (1 << P);
+    const vec2_t<R> x0 = a[e], x1 = a[e1];
+    a[e] = mk<R>(m00 * x0.x + m01 * x1.x, m00 * x0.y + m01 * x1.y);
+    a[e1] = mk<R>(m10 * x0.x + m11 * x1.x, m10 * x0.y + m11 * x1.y);
+  }
+}
+
+template <typename R, int NR, int P>
+__device__ __forceinline__ void bfly_slot(vec2_t<R> (&a)[1 << NR], vec2_t<R> c0, const vec2_t<R>* w, unsigned flags) {
+  // pair k of slot P: e = k with a zero inserted at bit P, e1 = e | 2^P
+#pragma unroll
+  for (int e = 0, k = 0; e < (1 << NR); ++e) {
+    if ((e >> P) & 1) continue;
+    const int e1 = e | (1 << P);
+    const vec2_t<R> s = mk<R>(a[e].x + a[e1].x, a[e].y + a[e1].y);
+    const vec2_t<R> d = mk<R>(a[e].x - a[e1].x, a[e].y - a[e1].y);
+    if (flags & F_C0ONE)
+      a[e] = s;
+    else if (flags & F_C0REAL)
+      a[e] = mk<R>(c0.x * s.x, c0.x * s.y);
+    else
+      a[e] = cmul<R>(c0, s);
+    a[e1] = cmul<R>(w[k], d);
+    ++k;
+  }
+}
+
+// element patterns: all elements, one register-bit condition, or two
+template <int NR, int P, int VP, int Q, int VQ>
+__device__ __forceinline__ constexpr bool pat_hit(int e) {
+  return (P < 0 || ((e >> P) & 1) == VP) && (Q < 0 || ((e >> Q) & 1) == VQ);
+}
+
+template <typename R, int NR, int P, int VP, int Q, int VQ>
+__device__ __forceinline__ void phase_pat(vec2_t<R> (&a)[1 << NR], vec2_t<R> c) {
+  if constexpr (P < NR && Q < NR) {
+#pragma unroll
+    for (int e = 0; e < (1 << NR); ++e)
+      if (pat_hit<NR, P, VP, Q, VQ>(e)) a[e] = cmul<R>(a[e], c);
+  }
+}
+
+// pattern codes (host pattern_of agrees): 0 = all; 1 + 2P + VP = one
+// condition; 9 + 4*pair(P<Q) + 2VP + VQ = two conditions
+#define SK_PAT_PAIR(P, Q, IDX)                                             \
+  case 9 + 4 * IDX + 0: phase_pat<R, NR, P, 0, Q, 0>(a, c); return true; \
+  case 9 + 4 * IDX + 1: phase_pat<R, NR, P, 0, Q, 1>(a, c); return true; \
+  case 9 + 4 * IDX + 2: phase_pat<R, NR, P, 1, Q, 0>(a, c); return true; \
+  case 9 + 4 * IDX + 3: phase_pat<R, NR, P, 1, Q, 1>(a, c); return true;
+
 template <typename R, int NR>
-__device__ __forceinline__ void apply_op(const DOp* __restrict__ op, vec2_t<R> (&a)[1 << NR], uint64_t gthr) {
-  const int kind = op->kind;
-  const uint64_t tmask = op->tmask, tval = op->tval;
-  if ((gthr & tmask) != tval) return;  // control outside the registers not satisfied
-  const uint32_t rmask = op->rmask, rval = op->rval;
-  if (kind == SK_OP_MAT) {
+__device__ __forceinline__ bool phase_dispatch(int pat, vec2_t<R> (&a)[1 << NR], vec2_t<R> c) {
+  switch (pat) {
+    case 0: phase_pat<R, NR, -1, 0, -1, 0>(a, c); return true;
+    case 1: phase_pat<R, NR, 0, 0, -1, 0>(a, c); return true;
+    case 2: phase_pat<R, NR, 0, 1, -1, 0>(a, c); return true;
+    case 3: phase_pat<R, NR, 1, 0, -1, 0>(a, c); return true;
+    case 4: phase_pat<R, NR, 1, 1, -1, 0>(a, c); return true;
+    case 5: phase_pat<R, NR, 2, 0, -1, 0>(a, c); return true;
+    case 6: phase_pat<R, NR, 2, 1, -1, 0>(a, c); return true;
+    case 7: phase_pat<R, NR, 3, 0, -1, 0>(a, c); return true;
+    case 8: phase_pat<R, NR, 3, 1, -1, 0>(a, c); return true;
+    SK_PAT_PAIR(0, 1, 0)
+    SK_PAT_PAIR(0, 2, 1)
+    SK_PAT_PAIR(0, 3, 2)
+    SK_PAT_PAIR(1, 2, 3)
+    SK_PAT_PAIR(1, 3, 4)
+    SK_PAT_PAIR(2, 3, 5)
+    default: return false;
+  }
+}
+#undef SK_PAT_PAIR
+
+#define SK_SLOT_SWITCH(slot, CALL)                  \
+  switch (slot) {                                   \
+    case 0: CALL(0); break;                         \
+    case 1: if (NR > 1) CALL((NR > 1 ? 1 : 0)); break; \
+    case 2: if (NR > 2) CALL((NR > 2 ? 2 : 0)); break; \
+    case 3: if (NR > 3) CALL((NR > 3 ? 3 : 0)); break; \
+    default: break;                                 \
+  }
+
+template <typename R, int NR>
+__device__ __forceinline__ void apply_kop(const KOp<R>* __restrict__ op, vec2_t<R> (&a)[1 << NR], uint64_t gthr) {
+  const uint4 raw = *reinterpret_cast<const uint4*>(&op->h);
+  KHdr h;
+  memcpy(&h, &raw, sizeof(h));
+  if ((h.flags & F_TPRED) && (gthr & op->tmask) != op->tval) return;
+  const uint32_t emask = h.emask;
+  const int kind = h.kind;
+  if (kind == K_BFLY) {
+    const vec2_t<R> c0 = mk<R>(op->m[0], op->m[1]);
+    vec2_t<R> c1 = mk<R>(op->m[4], op->m[5]);
+    if (h.flags & F_FOLD) c1 = cmul<R>(c1, thread_phase<R>(op->turn, gthr, h.lo, op->fmask));
+    vec2_t<R> w[1 << (NR - 1)];
+    if (h.flags & F_TABLE) {
+#pragma unroll
+      for (int k = 0; k < (1 << (NR - 1)); ++k) w[k] = cmul<R>(c1, mk<R>(op->tw[2 * k], op->tw[2 * k + 1]));
+    } else {
+#pragma unroll
+      for (int k = 0; k < (1 << (NR - 1)); ++k) w[k] = c1;
+    }
+    const unsigned fl = h.flags;
+#define SK_BF(P) bfly_slot<R, NR, P>(a, c0, w, fl)
+    SK_SLOT_SWITCH(h.slot, SK_BF)
+#undef SK_BF
+  } else if (kind == K_PHASE || kind == K_TPHASE) {
+    vec2_t<R> c;
+    if (kind == K_PHASE)
+      c = ((h.flags & F_QMASK) && (gthr & op->qmask)) ? mk<R>(op->m[2], op->m[3]) : mk<R>(op->m[0], op->m[1]);
+    else
+      c = thread_phase<R>(op->turn, gthr, h.lo, op->fmask);
+    if (!phase_dispatch<R, NR>(h.pat, a, c)) {
+#pragma unroll
+      for (int e = 0; e < (1 << NR); ++e)
+        if ((emask >> e) & 1u) a[e] = cmul<R>(a[e], c);
+    }
+  } else if (kind == K_MATR) {
+    const R m00 = op->m[0], m01 = op->m[2], m10 = op->m[4], m11 = op->m[6];
+#define SK_MR(P) matr_slot<R, NR, P>(a, m00, m01, m10, m11, emask)
+    SK_SLOT_SWITCH(h.slot, SK_MR)
+#undef SK_MR
+  } else {  // K_MAT
     Mat2<R> m;
-    m.m00 = mk<R>((R)op->m[0], (R)op->m[1]);
-    m.m01 = mk<R>((R)op->m[2], (R)op->m[3]);
-    m.m10 = mk<R>((R)op->m[4], (R)op->m[5]);
-    m.m11 = mk<R>((R)op->m[6], (R)op->m[7]);
-    switch (op->slot) {
-      case 0: mat_slot<R, NR, 0>(a, m, rmask, rval); break;
-      case 1: if (NR > 1) mat_slot<R, NR, (NR > 1 ? 1 : 0)>(a, m, rmask, rval); break;
-      case 2: if (NR > 2) mat_slot<R, NR, (NR > 2 ? 2 : 0)>(a, m, rmask, rval); break;
-      case 3: if (NR > 3) mat_slot<R, NR, (NR > 3 ? 3 : 0)>(a, m, rmask, rval); break;
-      default: break;
+    m.m00 = mk<R>(op->m[0], op->m[1]);
+    m.m01 = mk<R>(op->m[2], op->m[3]);
+    m.m10 = mk<R>(op->m[4], op->m[5]);
+    m.m11 = mk<R>(op->m[6], op->m[7]);
+    if (h.flags & F_FOLD) {
+      const vec2_t<R> tau = thread_phase<R>(op->turn, gthr, h.lo, op->fmask);
+      m.m10 = cmul<R>(m.m10, tau);
+      m.m11 = cmul<R>(m.m11, tau);
     }
-  } else if (kind == SK_OP_DIAG) {
-    const vec2_t<R> d0 = mk<R>((R)op->m[0], (R)op->m[1]);
-    const vec2_t<R> d1 = mk<R>((R)op->m[6], (R)op->m[7]);
-    const int slot = op->slot;
-    const bool tbit = (gthr & op->qmask) != 0;
-#pragma unroll
-    for (int e = 0; e < (1 << NR); ++e) {
-      if ((e & rmask) != rval) continue;
-      const bool b = slot >= 0 ? ((e >> slot) & 1) : tbit;
-      a[e] = cmul<R>(a[e], b ? d1 : d0);
-    }
-  } else {  // SK_OP_RAMP
-    const uint64_t fmask = op->nbits >= 64 ? ~0ull : ((1ull << op->nbits) - 1);
-    const uint64_t f = (gthr >> op->lo) & fmask;
-    double x = op->s * (double)f;
-    x -= 2.0 * floor(0.5 * x);
-    R sn, cs;
-    sincospi_r<R>(x, &sn, &cs);
-    const vec2_t<R> base = mk<R>(cs, sn);
-    vec2_t<R> w[NR];
-#pragma unroll
-    for (int p = 0; p < NR; ++p) w[p] = mk<R>((R)op->w[2 * p], (R)op->w[2 * p + 1]);
-#pragma unroll
-    for (int e = 0; e < (1 << NR); ++e) {
-      if ((e & rmask) != rval) continue;
-      vec2_t<R> ph = base;
-#pragma unroll
-      for (int p = 0; p < NR; ++p)
-        if ((e >> p) & 1) ph = cmul<R>(ph, w[p]);
-      a[e] = cmul<R>(a[e], ph);
-    }
+#define SK_M(P) mat_slot<R, NR, P>(a, m, emask)
+    SK_SLOT_SWITCH(h.slot, SK_M)
+#undef SK_M
   }
 }
 
 template <typename R, int NR>
 __global__ void __launch_bounds__(512, 2) k_sweep(vec2_t<R>* __restrict__ amps, const __grid_constant__ DSweep sw,
-                                                  const DOp* __restrict__ ops) {
+                                                  const KOp<R>* __restrict__ ops) {
+  using V = vec2_t<R>;
   extern __shared__ __align__(16) unsigned char smraw[];
-  vec2_t<R>* sm = reinterpret_cast<vec2_t<R>*>(smraw);
   constexpr int NE = 1 << NR;
-  constexpr int SB = sizeof(vec2_t<R>) == 8 ? 4 : 3;
-  const int T = sw.ntile;
-  const int TB = T - NR;
+  constexpr int SB = sizeof(V) == 8 ? 4 : 3;
   const uint32_t tid = threadIdx.x;
+  const uint64_t base = deposit(blockIdx.x, sw.brun, sw.nb);
 
-  // tile base: deposit blockIdx into the non-tile bits
-  uint64_t base = blockIdx.x;
-  for (int i = 0; i < T; ++i) base = insert0(base, sw.tile_bits[i]);
-
-  vec2_t<R> a[NE];
+  V a[NE];
   const int ns = sw.nstages;
   for (int s = 0; s < ns; ++s) {
     const DStage& st = sw.st[s];
-    uint64_t gthr = base;
-    uint32_t lthr = 0;
-    for (int i = 0; i < TB; ++i) {
-      if ((tid >> i) & 1u) {
-        gthr += st.thr_off[i];
-        lthr += st.thr_loc[i];
-      }
-    }
+    const uint64_t gthr = base | deposit(tid, st.grun, st.ng);
     if (s == 0) {
-      const vec2_t<R>* src = amps + gthr;
+      const char* p = reinterpret_cast<const char*>(amps + gthr);
 #pragma unroll
-      for (int e = 0; e < NE; ++e) {
-        uint64_t o = 0;
-#pragma unroll
-        for (int p = 0; p < NR; ++p)
-          if ((e >> p) & 1) o += st.reg_off[p];
-        a[e] = src[o];
+      for (int k = 0; k < NE; ++k) {
+        const int e = k ^ (k >> 1);
+        if (k) {
+          const int b = ctz_c(k);
+          p = ((e >> b) & 1) ? p + st.reg_goff[b] : p - st.reg_goff[b];
+        }
+        a[e] = *reinterpret_cast<const V*>(p);
       }
     } else {
       __syncthreads();
+      uint32_t so = swz<SB>((uint32_t)deposit(tid, st.lrun, st.nl)) * (uint32_t)sizeof(V);
 #pragma unroll
-      for (int e = 0; e < NE; ++e) {
-        uint32_t l = lthr;
-#pragma unroll
-        for (int p = 0; p < NR; ++p)
-          if ((e >> p) & 1) l += st.reg_loc[p];
-        a[e] = sm[swz<SB>(l)];
+      for (int k = 0; k < NE; ++k) {
+        const int e = k ^ (k >> 1);
+        if (k) so ^= st.reg_soff[ctz_c(k)];
+        a[e] = *reinterpret_cast<const V*>(smraw + so);
       }
     }
-    for (int o = st.op_begin; o < st.op_end; ++o) apply_op<R, NR>(ops + o, a, gthr);
+    for (int o = st.op_begin; o < st.op_end; ++o) apply_kop<R, NR>(ops + o, a, gthr);
     if (s == ns - 1) {
-      vec2_t<R>* dst = amps + gthr;
+      char* p = reinterpret_cast<char*>(amps + gthr);
 #pragma unroll
-      for (int e = 0; e < NE; ++e) {
-        uint64_t o = 0;
-#pragma unroll
-        for (int p = 0; p < NR; ++p)
-          if ((e >> p) & 1) o += st.reg_off[p];
-        dst[o] = a[e];
+      for (int k = 0; k < NE; ++k) {
+        const int e = k ^ (k >> 1);
+        if (k) {
+          const int b = ctz_c(k);
+          p = ((e >> b) & 1) ? p + st.reg_goff[b] : p - st.reg_goff[b];
+        }
+        *reinterpret_cast<V*>(p) = a[e];
       }
     } else {
       if (s > 0) __syncthreads();
+      uint32_t so = swz<SB>((uint32_t)deposit(tid, st.lrun, st.nl)) * (uint32_t)sizeof(V);
 #pragma unroll
-      for (int e = 0; e < NE; ++e) {
-        uint32_t l = lthr;
-#pragma unroll
-        for (int p = 0; p < NR; ++p)
-          if ((e >> p) & 1) l += st.reg_loc[p];
-        sm[swz<SB>(l)] = a[e];
+      for (int k = 0; k < NE; ++k) {
+        const int e = k ^ (k >> 1);
+        if (k) so ^= st.reg_soff[ctz_c(k)];
+        *reinterpret_cast<V*>(smraw + so) = a[e];
       }
     }
   }
@@ -224,6 +369,269 @@ constexpr int kNR64 = 3;
 constexpr int kMaxTile32 = 13;  // 64 KiB of shared memory per tile, 512 threads
 constexpr int kMaxTile64 = 12;
 
+// ---------------------------------------------------------------------------
+// host side: geometry (bit runs) and lowering of ABI ops into kernel ops
+// ---------------------------------------------------------------------------
+// runs mapping consecutive counter bits 0..k-1 to the ascending positions `dst`
+static int make_runs(const std::vector<int>& dst, Run* out) {
+  int n = 0;
+  for (size_t i = 0; i < dst.size(); ++i) {
+    if (n > 0 && out[n - 1].dst + out[n - 1].w == dst[i] && out[n - 1].src + out[n - 1].w == (int)i) {
+      out[n - 1].w++;
+    } else {
+      if (n >= kMaxRuns) return -1;
+      out[n].src = (uint8_t)i;
+      out[n].dst = (uint8_t)dst[i];
+      out[n].w = 1;
+      out[n].pad = 0;
+      ++n;
+    }
+  }
+  return n;
+}
+
+static uint64_t turn_of(double s) {
+  // exp(i pi s F) = exp(2 pi i F s/2): s/2 in 2^-64 turns, exact for |s| >~ 2^-11
+  int e = 0;
+  const double m = std::frexp(0.5 * s, &e);  // 0.5 s = m 2^e, |m| in [0.5, 1)
+  const int64_t M = (int64_t)std::ldexp(m, 53);
+  const int sh = e + 64 - 53;
+  if (sh >= 64) return 0;
+  if (sh >= 0) return (uint64_t)M << sh;
+  if (sh <= -63) return (uint64_t)(M < 0 ? -1 : 0);
+  return (uint64_t)(M >> -sh);
+}
+
+struct HostKOp {
+  int kind = K_PHASE, slot = -1, pat = -1;
+  uint32_t emask = 0, flags = 0;
+  int lo = 0, nbits = 0;
+  uint64_t tmask = 0, tval = 0, qmask = 0, turn = 0, fmask = 0;
+  double m[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  double tw[16] = {1, 0, 1, 0, 1, 0, 1, 0, 1, 0, 1, 0, 1, 0, 1, 0};
+};
+
+struct StageCtx {
+  int NR;
+  int slot_of[64];
+  uint64_t regmask;
+  uint64_t reg_off[kMaxR];
+};
+
+static uint32_t reg_pred_mask(const StageCtx& c, uint64_t cmask, uint64_t cval) {
+  uint32_t em = 0;
+  for (int e = 0; e < (1 << c.NR); ++e) {
+    bool ok = true;
+    for (int p = 0; p < c.NR; ++p) {
+      const uint64_t bit = c.reg_off[p];
+      if (cmask & bit) ok = ok && (((cval & bit) != 0) == (((e >> p) & 1) != 0));
+    }
+    if (ok) em |= 1u << e;
+  }
+  return em;
+}
+
+static uint32_t slot_mask(int NR, int p, int val) {
+  uint32_t em = 0;
+  for (int e = 0; e < (1 << NR); ++e)
+    if (((e >> p) & 1) == val) em |= 1u << e;
+  return em;
+}
+
+static bool is_one(double re, double im) { return re == 1.0 && im == 0.0; }
+
+static int pattern_of(int NR, uint32_t emask) {
+  const uint32_t all = (1u << (1 << NR)) - 1;
+  if (emask == all) return 0;
+  for (int p = 0; p < NR; ++p)
+    for (int v = 0; v < 2; ++v)
+      if (emask == slot_mask(NR, p, v)) return 1 + 2 * p + v;
+  int idx = 0;
+  for (int p = 0; p < 4; ++p)
+    for (int q = p + 1; q < 4; ++q, ++idx) {
+      if (q >= NR) continue;
+      for (int vp = 0; vp < 2; ++vp)
+        for (int vq = 0; vq < 2; ++vq)
+          if (emask == (slot_mask(NR, p, vp) & slot_mask(NR, q, vq))) return 9 + 4 * idx + 2 * vp + vq;
+    }
+  return -1;
+}
+
+static void set_pred(HostKOp& k, uint64_t tmask, uint64_t tval) {
+  k.tmask = tmask;
+  k.tval = tval;
+  if (tmask) k.flags |= F_TPRED;
+}
+
+// appends the kernel ops of ABI op `o` for one stage
+static int lower_op(const StageCtx& c, const sk_op& op, int o, int width, std::vector<HostKOp>& out,
+                    double* scale) {
+  if (op.ctrl_val & ~op.ctrl_mask) return set_error(SK_EVALUE, "op %d: ctrl_val outside ctrl_mask", o);
+  if (width < 64 && (op.ctrl_mask >> width)) return set_error(SK_EVALUE, "op %d: control beyond width %d", o, width);
+  const uint64_t tmask = op.ctrl_mask & ~c.regmask, tval = op.ctrl_val & ~c.regmask;
+  const uint32_t rpred = reg_pred_mask(c, op.ctrl_mask, op.ctrl_val);
+  if (op.kind == SK_OP_MAT) {
+    if (op.qubit < 0 || op.qubit >= width || c.slot_of[op.qubit] < 0)
+      return set_error(SK_EVALUE, "op %d: MAT target %d is not a register bit of its stage", o, op.qubit);
+    if ((op.ctrl_mask >> op.qubit) & 1ull) return set_error(SK_EVALUE, "op %d: target %d is a control", o, op.qubit);
+    HostKOp k;
+    const int p = c.slot_of[op.qubit];
+    bool real = true;
+    for (int i = 1; i < 8; i += 2) real = real && op.m[i] == 0.0;
+    k.kind = real ? K_MATR : K_MAT;
+    k.slot = p;
+    k.emask = rpred & slot_mask(c.NR, p, 0);
+    set_pred(k, tmask, tval);
+    for (int i = 0; i < 8; ++i) k.m[i] = op.m[i];
+    const bool bfly = op.m[0] == op.m[2] && op.m[1] == op.m[3] && op.m[4] == -op.m[6] && op.m[5] == -op.m[7];
+    if (bfly && k.emask == slot_mask(c.NR, p, 0)) {  // H-like: y0 = c0 (a0 + a1), y1 = c1 (a0 - a1)
+      k.kind = K_BFLY;
+      k.m[2] = k.m[3] = k.m[6] = k.m[7] = 0;
+      if (op.m[1] == 0.0) k.flags |= F_C0REAL;
+      const double c0r = op.m[0], c0i = op.m[1], den = c0r * c0r + c0i * c0i;
+      if (tmask == 0 && den > 0 && scale != nullptr) {
+        // an unpredicated butterfly is c0 * [[1, 1], [c1/c0, -c1/c0]]: defer the scalar c0
+        const double qr = (op.m[4] * c0r + op.m[5] * c0i) / den, qi = (op.m[5] * c0r - op.m[4] * c0i) / den;
+        const double sr = scale[0] * c0r - scale[1] * c0i, si = scale[0] * c0i + scale[1] * c0r;
+        scale[0] = sr;
+        scale[1] = si;
+        k.m[0] = 1;
+        k.m[1] = 0;
+        k.m[4] = qr;
+        k.m[5] = qi;
+        k.flags |= F_C0ONE;
+      }
+    }
+    if (k.emask) out.push_back(k);
+    return SK_OK;
+  }
+  if (op.kind == SK_OP_DIAG) {
+    if (op.qubit < 0 || op.qubit >= width) return set_error(SK_EVALUE, "op %d: DIAG qubit %d out of range", o, op.qubit);
+    if ((op.ctrl_mask >> op.qubit) & 1ull) return set_error(SK_EVALUE, "op %d: qubit %d is a control", o, op.qubit);
+    const int p = c.slot_of[op.qubit];
+    if (p >= 0) {
+      for (int v = 0; v < 2; ++v) {
+        const double re = op.m[v ? 6 : 0], im = op.m[v ? 7 : 1];
+        if (is_one(re, im)) continue;
+        HostKOp k;
+        k.kind = K_PHASE;
+        k.emask = rpred & slot_mask(c.NR, p, v);
+        set_pred(k, tmask, tval);
+        k.m[0] = k.m[2] = re;
+        k.m[1] = k.m[3] = im;
+        if (k.emask) out.push_back(k);
+      }
+    } else {
+      if (is_one(op.m[0], op.m[1]) && is_one(op.m[6], op.m[7])) return SK_OK;
+      HostKOp k;
+      k.kind = K_PHASE;
+      k.emask = rpred;
+      set_pred(k, tmask, tval);
+      k.qmask = 1ull << op.qubit;
+      k.flags |= F_QMASK;
+      k.m[0] = op.m[0];
+      k.m[1] = op.m[1];
+      k.m[2] = op.m[6];
+      k.m[3] = op.m[7];
+      if (k.emask) out.push_back(k);
+    }
+    return SK_OK;
+  }
+  if (op.kind == SK_OP_RAMP) {
+    if (op.qubit < 0 || op.nbits < 1 || op.nbits > 62 || op.qubit + op.nbits > width)
+      return set_error(SK_EVALUE, "op %d: bad RAMP field at bit %d", o, op.qubit);
+    const uint64_t field = ((1ull << op.nbits) - 1) << op.qubit;
+    if (op.ctrl_mask & field) return set_error(SK_EVALUE, "op %d: RAMP field overlaps its controls", o);
+    const double s = op.m[0];
+    const uint64_t turn = turn_of(s);
+    // thread part: one per-thread phase (register bits are zero in gthr)
+    bool fold = false;
+    if (!out.empty() && tmask == 0) {  // fold into a preceding unpredicated MAT/BFLY on the control slot
+      HostKOp& prev = out.back();
+      if ((prev.kind == K_MAT || prev.kind == K_MATR || prev.kind == K_BFLY) && prev.tmask == 0 &&
+          !(prev.flags & F_FOLD) && prev.emask == slot_mask(c.NR, prev.slot, 0) &&
+          rpred == slot_mask(c.NR, prev.slot, 1)) {
+        if (prev.kind == K_MATR) prev.kind = K_MAT;
+        prev.flags |= F_FOLD;
+        prev.lo = op.qubit;
+        prev.nbits = op.nbits;
+        prev.fmask = (1ull << op.nbits) - 1;
+        prev.turn = turn;
+        fold = true;
+      }
+    }
+    const bool table = fold && out.back().kind == K_BFLY;
+    const int jslot = fold ? out.back().slot : -1;
+    if (!fold && rpred) {
+      HostKOp t;
+      t.kind = K_TPHASE;
+      t.emask = rpred;
+      set_pred(t, tmask, tval);
+      t.lo = op.qubit;
+      t.nbits = op.nbits;
+      t.fmask = (1ull << op.nbits) - 1;
+      t.turn = turn;
+      out.push_back(t);
+    }
+    // register part: constant phases on elements whose field register bit is set
+    for (int p = 0; p < c.NR; ++p) {
+      const uint64_t bit = c.reg_off[p];
+      if (!(bit & field)) continue;
+      const int q = __builtin_ctzll(bit);
+      double x = s * (double)(1ull << (q - op.qubit));
+      x -= 2.0 * std::floor(0.5 * x);
+      if (x == 0.0) continue;
+      const double wr = std::cos(M_PI * x), wi = std::sin(M_PI * x);
+      if (table) {  // multiply into the butterfly's row-1 twiddle of every pair whose e1 has bit p
+        HostKOp& bf = out.back();
+        for (int k = 0; k < (1 << (c.NR - 1)); ++k) {
+          const int e1 = (int)(insert0((uint64_t)k, jslot) | (1u << jslot));
+          if (!((e1 >> p) & 1)) continue;
+          const double r = bf.tw[2 * k] * wr - bf.tw[2 * k + 1] * wi, i = bf.tw[2 * k] * wi + bf.tw[2 * k + 1] * wr;
+          bf.tw[2 * k] = r;
+          bf.tw[2 * k + 1] = i;
+        }
+        bf.flags |= F_TABLE;
+        continue;
+      }
+      HostKOp k;
+      k.kind = K_PHASE;
+      k.emask = rpred & slot_mask(c.NR, p, 1);
+      set_pred(k, tmask, tval);
+      k.m[0] = k.m[2] = wr;
+      k.m[1] = k.m[3] = wi;
+      if (k.emask) out.push_back(k);
+    }
+    return SK_OK;
+  }
+  return set_error(SK_EVALUE, "op %d: unknown kind %d", o, op.kind);
+}
+
+template <typename R>
+static void pack_kops(std::vector<HostKOp>& h, std::vector<unsigned char>& buf, int NR) {
+  buf.assign(sizeof(KOp<R>) * h.size(), 0);
+  KOp<R>* k = reinterpret_cast<KOp<R>*>(buf.data());
+  for (size_t i = 0; i < h.size(); ++i) {
+    if (h[i].kind == K_PHASE || h[i].kind == K_TPHASE) h[i].pat = pattern_of(NR, h[i].emask);
+    KOp<R> x{};
+    x.h.kind = (int16_t)h[i].kind;
+    x.h.slot = (int8_t)h[i].slot;
+    x.h.pat = (int8_t)h[i].pat;
+    x.h.emask = (uint16_t)h[i].emask;
+    x.h.lo = (uint8_t)h[i].lo;
+    x.h.nbits = (uint8_t)h[i].nbits;
+    x.h.flags = h[i].flags;
+    x.tmask = h[i].tmask;
+    x.tval = h[i].tval;
+    x.qmask = h[i].qmask;
+    x.turn = h[i].turn;
+    x.fmask = h[i].fmask;
+    for (int j = 0; j < 8; ++j) x.m[j] = (R)h[i].m[j];
+    for (int j = 0; j < 16; ++j) x.tw[j] = (R)h[i].tw[j];
+    k[i] = x;
+  }
+}
+
 }  // namespace sk
 
 struct sk_program {
@@ -232,8 +640,8 @@ struct sk_program {
   int device = 0;
   int nr = 0;
   std::vector<sk::DSweep> sweeps;
-  sk::DOp* d_ops = nullptr;
-  int nops = 0;
+  void* d_ops = nullptr;
+  int nkops = 0;
 };
 
 using namespace sk;
@@ -252,8 +660,90 @@ static int launch_sweeps(sk_state* s, const sk_program* p, int first, int count,
     const unsigned threads = 1u << (T - NR);
     const size_t smem = ((size_t)1 << T) * sizeof(vec2_t<R>);
     if (tiles > 0x7fffffffull) return set_error(SK_EVALUE, "too many tiles (%d bits outside the tile)", s->width - T);
-    k_sweep<R, NR><<<(unsigned)tiles, threads, smem, c->stream>>>((vec2_t<R>*)s->d, d, p->d_ops);
+    k_sweep<R, NR><<<(unsigned)tiles, threads, smem, c->stream>>>((vec2_t<R>*)s->d, d, (const KOp<R>*)p->d_ops);
     SK_CHECK_LAUNCH();
+  }
+  return SK_OK;
+}
+
+static int lower_program(int width, int dtype, const sk_sweep* sweeps, int nsweeps, const sk_op* ops, int nops,
+                         std::vector<DSweep>& dsw, std::vector<HostKOp>& kops) {
+  if (dtype != SK_C64 && dtype != SK_C128) return set_error(SK_EVALUE, "bad dtype %d", dtype);
+  const int NR = dtype == SK_C64 ? kNR32 : kNR64;
+  const int maxT = dtype == SK_C64 ? kMaxTile32 : kMaxTile64;
+  const uint32_t esz = dtype == SK_C64 ? 8 : 16;
+  if (width < NR || width > 40) return set_error(SK_EVALUE, "fused program needs %d <= width <= 40", NR);
+  if (nsweeps < 0 || nops < 0) return set_error(SK_EVALUE, "negative counts");
+  std::vector<int> op_seen(nops, 0);
+  for (int si = 0; si < nsweeps; ++si) {
+    const sk_sweep& sw = sweeps[si];
+    DSweep d{};
+    const int T = sw.ntile;
+    if (T < NR || T > maxT || T > width) return set_error(SK_EVALUE, "sweep %d: bad tile bit count %d", si, T);
+    int local_of[64];
+    for (int b = 0; b < 64; ++b) local_of[b] = -1;
+    uint64_t tilemask = 0;
+    for (int i = 0; i < T; ++i) {
+      const int b = sw.tile_bits[i];
+      if (b < 0 || b >= width || (i > 0 && b <= sw.tile_bits[i - 1]))
+        return set_error(SK_EVALUE, "sweep %d: tile bits must be ascending and < width (bit %d)", si, b);
+      local_of[b] = i;
+      tilemask |= 1ull << b;
+    }
+    d.ntile = T;
+    std::vector<int> nontile;
+    for (int b = 0; b < width; ++b)
+      if (!((tilemask >> b) & 1ull)) nontile.push_back(b);
+    d.nb = make_runs(nontile, d.brun);
+    if (d.nb < 0) return set_error(SK_EVALUE, "sweep %d: non-tile bits too fragmented", si);
+    if (sw.nstages < 1 || sw.nstages > kMaxS) return set_error(SK_EVALUE, "sweep %d: bad stage count %d", si, sw.nstages);
+    d.nstages = sw.nstages;
+    double scale[2] = {1.0, 0.0};
+    for (int s = 0; s < sw.nstages; ++s) {
+      DStage& st = d.st[s];
+      StageCtx c{};
+      c.NR = NR;
+      c.regmask = 0;
+      for (int b = 0; b < 64; ++b) c.slot_of[b] = -1;
+      for (int p = 0; p < NR; ++p) {
+        const int q = sw.reg_bits[s][p];
+        if (q < 0 || q >= width || local_of[q] < 0 || ((c.regmask >> q) & 1ull))
+          return set_error(SK_EVALUE, "sweep %d: register bit %d not a distinct tile bit", si, q);
+        c.regmask |= 1ull << q;
+        c.slot_of[q] = p;
+        c.reg_off[p] = 1ull << q;
+        st.reg_goff[p] = (uint64_t)esz << q;
+        st.reg_soff[p] = (esz == 8 ? swz<4>(1u << local_of[q]) : swz<3>(1u << local_of[q])) * esz;
+      }
+      std::vector<int> gdst, ldst;
+      for (int i = 0; i < T; ++i) {
+        const int b = sw.tile_bits[i];
+        if ((c.regmask >> b) & 1ull) continue;
+        gdst.push_back(b);
+        ldst.push_back(i);
+      }
+      st.ng = make_runs(gdst, st.grun);
+      st.nl = make_runs(ldst, st.lrun);
+      if (st.ng < 0 || st.nl < 0) return set_error(SK_EVALUE, "sweep %d: thread bits too fragmented", si);
+      const int ob = sw.op_begin[s], oe = sw.op_begin[s + 1];
+      if (ob < 0 || oe < ob || oe > nops) return set_error(SK_EVALUE, "sweep %d: bad op range in stage %d", si, s);
+      st.op_begin = (int)kops.size();
+      for (int o = ob; o < oe; ++o) {
+        if (op_seen[o]) return set_error(SK_EVALUE, "op %d used by two stages (sweep %d)", o, si);
+        op_seen[o] = 1;
+        SK_TRY(lower_op(c, ops[o], o, width, kops, scale));
+      }
+      if (s == sw.nstages - 1 && !(scale[0] == 1.0 && scale[1] == 0.0)) {  // deferred butterfly scalars
+        HostKOp k;
+        k.kind = K_PHASE;
+        k.emask = (1u << (1 << NR)) - 1;
+        k.m[0] = k.m[2] = scale[0];
+        k.m[1] = k.m[3] = scale[1];
+        kops.push_back(k);
+      }
+      st.op_end = (int)kops.size();
+    }
+    dsw.push_back(d);
   }
   return SK_OK;
 }
@@ -268,127 +758,27 @@ int sk_program_reg_bits(int dtype, int* nreg) {
 
 int sk_program_create(int width, int dtype, int device, const sk_sweep* sweeps, int nsweeps, const sk_op* ops,
                       int nops, sk_program** out) {
-  if (dtype != SK_C64 && dtype != SK_C128) return set_error(SK_EVALUE, "bad dtype %d", dtype);
+  std::vector<HostKOp> kops;
+  std::vector<DSweep> dsw;
+  SK_TRY(lower_program(width, dtype, sweeps, nsweeps, ops, nops, dsw, kops));
   const int NR = dtype == SK_C64 ? kNR32 : kNR64;
-  const int maxT = dtype == SK_C64 ? kMaxTile32 : kMaxTile64;
-  if (width < NR || width > 40) return set_error(SK_EVALUE, "fused program needs %d <= width <= 40", NR);
-  if (nsweeps < 0 || nops < 0) return set_error(SK_EVALUE, "negative counts");
-  std::vector<DOp> dops(nops);
-  std::vector<int> op_seen(nops, 0);
+  DevCtx* c;
+  SK_TRY(ctx_get(device, &c));
+  std::vector<unsigned char> buf;
+  if (dtype == SK_C64)
+    pack_kops<float>(kops, buf, NR);
+  else
+    pack_kops<double>(kops, buf, NR);
   sk_program* prog = new sk_program();
   prog->width = width;
   prog->dtype = dtype;
   prog->device = device;
   prog->nr = NR;
-  auto fail = [&](int code, const char* msg, int a, int b) {
-    delete prog;
-    return set_error(code, msg, a, b);
-  };
-  for (int si = 0; si < nsweeps; ++si) {
-    const sk_sweep& sw = sweeps[si];
-    DSweep d{};
-    const int T = sw.ntile;
-    if (T < NR || T > maxT || T > width) return fail(SK_EVALUE, "sweep %d: bad tile bit count %d", si, T);
-    int local_of[64];
-    for (int b = 0; b < 64; ++b) local_of[b] = -1;
-    for (int i = 0; i < T; ++i) {
-      const int b = sw.tile_bits[i];
-      if (b < 0 || b >= width || (i > 0 && b <= sw.tile_bits[i - 1]))
-        return fail(SK_EVALUE, "sweep %d: tile bits must be ascending and < width (bit %d)", si, b);
-      local_of[b] = i;
-      d.tile_bits[i] = b;
-    }
-    d.ntile = T;
-    if (sw.nstages < 1 || sw.nstages > kMaxS) return fail(SK_EVALUE, "sweep %d: bad stage count %d", si, sw.nstages);
-    d.nstages = sw.nstages;
-    for (int s = 0; s < sw.nstages; ++s) {
-      DStage& st = d.st[s];
-      uint64_t regmask = 0;
-      int slot_of[64];
-      for (int b = 0; b < 64; ++b) slot_of[b] = -1;
-      for (int p = 0; p < NR; ++p) {
-        const int q = sw.reg_bits[s][p];
-        if (q < 0 || q >= width || local_of[q] < 0 || ((regmask >> q) & 1ull))
-          return fail(SK_EVALUE, "sweep %d: register bit %d not a distinct tile bit", si, q);
-        regmask |= 1ull << q;
-        slot_of[q] = p;
-        st.reg_off[p] = 1ull << q;
-        st.reg_loc[p] = 1u << local_of[q];
-      }
-      int ti = 0;
-      for (int i = 0; i < T; ++i) {
-        const int b = sw.tile_bits[i];
-        if ((regmask >> b) & 1ull) continue;
-        st.thr_off[ti] = 1ull << b;
-        st.thr_loc[ti] = 1u << i;
-        ++ti;
-      }
-      const int ob = sw.op_begin[s], oe = sw.op_begin[s + 1];
-      if (ob < 0 || oe < ob || oe > nops) return fail(SK_EVALUE, "sweep %d: bad op range in stage %d", si, s);
-      st.op_begin = ob;
-      st.op_end = oe;
-      for (int o = ob; o < oe; ++o) {
-        if (op_seen[o]) return fail(SK_EVALUE, "op %d used by two stages (sweep %d)", o, si);
-        op_seen[o] = 1;
-        const sk_op& op = ops[o];
-        DOp& x = dops[o];
-        x.kind = op.kind;
-        if (op.ctrl_val & ~op.ctrl_mask) return fail(SK_EVALUE, "op %d: ctrl_val outside ctrl_mask (sweep %d)", o, si);
-        if (width < 64 && (op.ctrl_mask >> width)) return fail(SK_EVALUE, "op %d: control beyond width %d", o, width);
-        x.tmask = op.ctrl_mask & ~regmask;
-        x.tval = op.ctrl_val & ~regmask;
-        x.rmask = 0;
-        x.rval = 0;
-        for (int p = 0; p < NR; ++p) {
-          const int q = sw.reg_bits[s][p];
-          if ((op.ctrl_mask >> q) & 1ull) {
-            x.rmask |= 1u << p;
-            if ((op.ctrl_val >> q) & 1ull) x.rval |= 1u << p;
-          }
-        }
-        for (int k = 0; k < 8; ++k) x.m[k] = op.m[k];
-        if (op.kind == SK_OP_MAT) {
-          if (op.qubit < 0 || op.qubit >= width || slot_of[op.qubit] < 0)
-            return fail(SK_EVALUE, "op %d: MAT target %d is not a register bit of its stage", o, op.qubit);
-          if ((op.ctrl_mask >> op.qubit) & 1ull) return fail(SK_EVALUE, "op %d: target %d is a control", o, op.qubit);
-          x.slot = slot_of[op.qubit];
-        } else if (op.kind == SK_OP_DIAG) {
-          if (op.qubit < 0 || op.qubit >= width) return fail(SK_EVALUE, "op %d: DIAG qubit %d out of range", o, op.qubit);
-          if ((op.ctrl_mask >> op.qubit) & 1ull) return fail(SK_EVALUE, "op %d: qubit %d is a control", o, op.qubit);
-          x.slot = slot_of[op.qubit];
-          x.qmask = x.slot >= 0 ? 0 : (1ull << op.qubit);
-        } else if (op.kind == SK_OP_RAMP) {
-          if (op.qubit < 0 || op.nbits < 1 || op.qubit + op.nbits > width)
-            return fail(SK_EVALUE, "op %d: bad RAMP field at bit %d", o, op.qubit);
-          x.slot = -1;
-          x.lo = op.qubit;
-          x.nbits = op.nbits;
-          x.s = op.m[0];
-          const uint64_t fmask = (1ull << op.nbits) - 1;
-          for (int p = 0; p < NR; ++p) {
-            const uint64_t f = (st.reg_off[p] >> op.qubit) & fmask;
-            double xx = op.m[0] * (double)f;
-            xx -= 2.0 * std::floor(0.5 * xx);
-            x.w[2 * p] = std::cos(M_PI * xx);
-            x.w[2 * p + 1] = std::sin(M_PI * xx);
-          }
-        } else {
-          return fail(SK_EVALUE, "op %d: unknown kind %d", o, op.kind);
-        }
-      }
-    }
-    prog->sweeps.push_back(d);
-  }
-  DevCtx* c;
-  int rc = ctx_get(device, &c);
-  if (rc != SK_OK) {
-    delete prog;
-    return rc;
-  }
-  prog->nops = nops;
-  if (nops > 0) {
-    cudaError_t e = cudaMalloc(&prog->d_ops, sizeof(DOp) * nops);
-    if (e == cudaSuccess) e = cudaMemcpy(prog->d_ops, dops.data(), sizeof(DOp) * nops, cudaMemcpyHostToDevice);
+  prog->sweeps = std::move(dsw);
+  prog->nkops = (int)kops.size();
+  if (!buf.empty()) {
+    cudaError_t e = cudaMalloc(&prog->d_ops, buf.size());
+    if (e == cudaSuccess) e = cudaMemcpy(prog->d_ops, buf.data(), buf.size(), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
       cudaGetLastError();
       if (prog->d_ops) cudaFree(prog->d_ops);
@@ -397,6 +787,32 @@ int sk_program_create(int width, int dtype, int device, const sk_sweep* sweeps, 
     }
   }
   *out = prog;
+  return SK_OK;
+}
+
+int sk_program_lower(int width, int dtype, const sk_sweep* sweeps, int nsweeps, const sk_op* ops, int nops,
+                     int64_t* ints, double* reals, int cap, int* count, int* stage_ops) {
+  std::vector<HostKOp> kops;
+  std::vector<DSweep> dsw;
+  SK_TRY(lower_program(width, dtype, sweeps, nsweeps, ops, nops, dsw, kops));
+  const int NR = dtype == SK_C64 ? kNR32 : kNR64;
+  for (auto& k : kops)
+    if (k.kind == K_PHASE || k.kind == K_TPHASE) k.pat = pattern_of(NR, k.emask);
+  *count = (int)kops.size();
+  if ((int)kops.size() > cap) return set_error(SK_EVALUE, "need room for %d kernel ops", (int)kops.size());
+  for (size_t i = 0; i < kops.size(); ++i) {
+    const HostKOp& k = kops[i];
+    int64_t* x = ints + 12 * i;
+    x[0] = k.kind; x[1] = k.slot; x[2] = k.pat; x[3] = k.emask; x[4] = k.flags; x[5] = k.lo; x[6] = k.nbits;
+    x[7] = (int64_t)k.tmask; x[8] = (int64_t)k.tval; x[9] = (int64_t)k.qmask; x[10] = (int64_t)k.turn;
+    x[11] = (int64_t)k.fmask;
+    for (int j = 0; j < 8; ++j) reals[24 * i + j] = k.m[j];
+    for (int j = 0; j < 16; ++j) reals[24 * i + 8 + j] = k.tw[j];
+  }
+  for (int si = 0; si < nsweeps; ++si)
+    for (int st = 0; st <= SK_MAX_STAGES; ++st)
+      stage_ops[si * (SK_MAX_STAGES + 1) + st] =
+          st < dsw[si].nstages ? dsw[si].st[st].op_begin : (st == dsw[si].nstages ? dsw[si].st[st - 1].op_end : -1);
   return SK_OK;
 }
 

@@ -616,7 +616,7 @@ int sk_device_count(void) {
 int sk_set_stream(int device, uint64_t stream) {
   DevCtx* c;
   SK_TRY(ctx_get(device, &c));
-  c->stream = stream ? (cudaStream_t)stream : c->own_stream;
+  c->stream = stream == SK_OWN_STREAM ? c->own_stream : (cudaStream_t)stream;
   return SK_OK;
 }
 

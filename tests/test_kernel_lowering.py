@@ -1,0 +1,149 @@
+"""Host-side lowering of fused programs into kernel ops (sk_program_lower,
+no device needed), emulated with NumPy exactly as k_sweep applies them
+(element masks, thread predicates, butterflies, folded fixed-point phases),
+must reproduce the oracle's gate-by-gate dense loop.  CPU only."""
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import numpy as np
+import pytest
+
+from oracle import ket_oracle as O
+from paper_2304_14969_b200 import _lib, fusion
+from paper_2304_14969_b200.circuit import (Circuit, Gate, build_qft, build_random_circuit, cp, cx, gate_matrix, h,
+                                           rz, swap, u3)
+
+from conftest import random_state
+
+K_MAT, K_MATR, K_PHASE, K_TPHASE, K_BFLY = range(5)
+F_TPRED, F_QMASK, F_C0REAL, F_FOLD, F_TABLE, F_C0ONE = 1, 2, 4, 8, 16, 32
+NS = _lib.SK_MAX_STAGES + 1
+
+
+def lower(plan: fusion.Plan):
+    sweeps, ops, nops = fusion.to_c(plan)
+    cap = 64 * max(1, nops) + 64
+    ints = (C.c_int64 * (12 * cap))()
+    reals = (C.c_double * (24 * cap))()
+    count = C.c_int()
+    stage_ops = (C.c_int * (NS * len(plan.sweeps)))()
+    _lib.call("sk_program_lower", plan.width, _lib.DTYPES[plan.dtype], sweeps, len(plan.sweeps), ops, nops, ints,
+              reals, cap, C.byref(count), stage_ops)
+    n = count.value
+    I = np.frombuffer(ints, dtype=np.int64)[: 12 * n].reshape(n, 12)
+    Rl = np.frombuffer(reals, dtype=np.float64)[: 24 * n].reshape(n, 24)
+    return I, Rl, np.frombuffer(stage_ops, dtype=np.int32).reshape(len(plan.sweeps), NS)
+
+
+def tau(turn, gthr, lo, fmask):
+    f = (gthr >> np.uint64(lo)) & np.uint64(fmask)
+    t = f * np.uint64(turn & 0xFFFFFFFFFFFFFFFF)  # wraps mod 2^64 like the kernel
+    return np.exp(2j * np.pi * (t.astype(np.float64) / 2.0 ** 64))
+
+
+def emulate(plan: fusion.Plan, amps: np.ndarray) -> np.ndarray:
+    I, Rl, stage_ops = lower(plan)
+    n = plan.width
+    g = np.arange(1 << n, dtype=np.uint64)
+    for si, sp in enumerate(plan.sweeps):
+        for st, st_plan in enumerate(sp.stages):
+            regs = st_plan.reg_bits
+            regmask = sum(1 << q for q in regs)
+            e_of = np.zeros(1 << n, dtype=np.int64)
+            for p, q in enumerate(regs):
+                e_of |= (((g >> np.uint64(q)) & np.uint64(1)).astype(np.int64)) << p
+            gthr = g & np.uint64(~regmask & ((1 << 64) - 1))
+            for k in range(stage_ops[si, st], stage_ops[si, st + 1]):
+                kind, slot, pat, emask, flags, lo, nbits, tmask, tval, qmask, turn, fmask = (int(v) for v in I[k])
+                m = Rl[k]
+                ok = np.ones(1 << n, dtype=bool)
+                if flags & F_TPRED:
+                    ok = (gthr & np.uint64(tmask & (2**64 - 1))) == np.uint64(tval & (2**64 - 1))
+                inmask = ((emask >> e_of) & 1).astype(bool) & ok
+                if kind in (K_PHASE, K_TPHASE):
+                    if kind == K_PHASE:
+                        c = np.full(1 << n, complex(m[0], m[1]))
+                        if flags & F_QMASK:
+                            c = np.where((gthr & np.uint64(qmask)) != 0, complex(m[2], m[3]), c)
+                    else:
+                        c = tau(turn, gthr, lo, fmask)
+                    amps[inmask] *= c[inmask]
+                else:
+                    q = regs[slot]
+                    base = inmask & (((g >> np.uint64(q)) & np.uint64(1)) == 0)
+                    i0 = np.nonzero(base)[0]
+                    i1 = i0 | (1 << q)
+                    a0, a1 = amps[i0].copy(), amps[i1].copy()
+                    if kind == K_BFLY:
+                        c0 = complex(m[0], m[1])
+                        c1 = np.full(i0.size, complex(m[4], m[5]))
+                        if flags & F_FOLD:
+                            c1 = c1 * tau(turn, gthr[i0], lo, fmask)
+                        if flags & F_TABLE:
+                            e0 = e_of[i0]
+                            kk = (e0 & ((1 << slot) - 1)) | ((e0 >> (slot + 1)) << slot)
+                            tw = m[8::2] + 1j * m[9::2]
+                            c1 = c1 * tw[kk]
+                        amps[i0] = (a0 + a1) if flags & F_C0ONE else c0 * (a0 + a1)
+                        amps[i1] = c1 * (a0 - a1)
+                    else:
+                        m00, m01 = complex(m[0], m[1]), complex(m[2], m[3])
+                        m10, m11 = complex(m[4], m[5]), complex(m[6], m[7])
+                        if flags & F_FOLD:
+                            t = tau(turn, gthr[i0], lo, fmask)
+                            m10, m11 = m10 * t, m11 * t
+                        amps[i0] = m00 * a0 + m01 * a1
+                        amps[i1] = m10 * a0 + m11 * a1
+    return O.permute_qubits(amps, plan.order)
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("n", [5, 9, 14])
+def test_qft_lowering(rng, dtype, n):
+    x = random_state(n, rng)
+    plan = fusion.plan_circuit(build_qft(n), dtype=dtype, tile_bits=min(n, 8), low_bits=min(3, n - 4))
+    got = emulate(plan, x.copy())
+    assert np.max(np.abs(got - O.dft_oracle(x))) < 1e-12
+
+
+def test_qft_lowering_uses_butterflies_and_folds():
+    plan = fusion.plan_circuit(build_qft(16), dtype="c64")
+    I, _, _ = lower(plan)
+    kinds = list(I[:, 0])
+    assert kinds.count(K_BFLY) == 16
+    assert kinds.count(K_TPHASE) == 0  # every RAMP's thread part folded into its H
+    assert sum(1 for r in I if r[0] == K_PHASE and r[2] < 0) == 0  # all phases hit a specialised pattern
+    # register-part phases ride in the butterflies' twiddle tables: only the
+    # per-sweep deferred 1/sqrt(2)^L scalars (pattern 0) and the lone CP(0,1)
+    # (a one-gate fan, not a RAMP) remain as phase ops
+    assert sum(1 for r in I if r[0] == K_PHASE and r[2] == 0) == len(plan.sweeps)
+    assert kinds.count(K_PHASE) == len(plan.sweeps) + 1
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_random_circuit_lowering(dtype):
+    c = build_random_circuit(11, 6, 9)
+    x = np.zeros(1 << 11, complex)
+    x[0] = 1
+    plan = fusion.plan_circuit(c, dtype=dtype, tile_bits=8, low_bits=3)
+    got = emulate(plan, x)
+    want = O.dense_run(c.gates, np.eye(1, 1 << 11, dtype=complex).ravel(), gate_matrix)
+    assert np.max(np.abs(got - want)) < 1e-12
+
+
+def test_mixed_controls_phases_and_general_ramps(rng):
+    n = 10
+    gates = [h(0), cx(0, 9), swap(1, 8), u3(0.3, 0.2, 0.1, 8), rz(0.4, 3), cp(0.7, 3, 9),
+             Gate("y", (5,), controls=(2, 7), polarity=(1, 0)), Gate("z", (6,), controls=(1, 4), polarity=(0, 1)),
+             h(4), Gate("p", (2,), (0.9,), controls=(8,), polarity=(0,))]
+    gates += [cp(-0.37 * (1 << k), 6 - k, 6) for k in range(1, 6)]  # a general (non-dyadic) ramp
+    gates += [cp(math.pi / (1 << k), 9 - k, 9) for k in range(1, 4)] + [h(9), h(6)]
+    c = Circuit(n, tuple(gates))
+    x = random_state(n, rng)
+    want = O.dense_run(c.gates, x.copy(), gate_matrix)
+    for dtype in ("c64", "c128"):
+        plan = fusion.plan_circuit(c, dtype=dtype, tile_bits=7, low_bits=2)
+        got = emulate(plan, x.copy())
+        assert np.max(np.abs(got - want)) < 1e-12
