@@ -1,0 +1,8 @@
+set -x
+for m in 0 1; do
+SK_SWEEP_PIPE=$m timeout 300 python scripts/tune_qft.py 27 c64 > gpurun_out/tune_c64_p$m.log 2>&1
+done
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_sweep -s 9 -c 1 -o gpurun_out/prof2 -f python bench.py --steps 1 --warmup 3 --no-cpu > gpurun_out/ncu2.log 2>&1
+timeout 900 python -m pytest tests -q -m gpu -p no:cacheprovider -x > gpurun_out/pytest_gpu.log 2>&1
+tail -3 gpurun_out/pytest_gpu.log
+for f in gpurun_out/tune_c64_p*.log; do echo == $f; cat $f; done
