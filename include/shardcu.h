@@ -156,6 +156,8 @@ int sk_sample(const sk_state* s, const double* uniforms, int64_t k, int64_t* out
 #define SK_OP_MAT 0   /* 2x2 matrix on register slot `slot`, predicated      */
 #define SK_OP_DIAG 1  /* diag(d0, d1) on global qubit `qubit`, predicated     */
 #define SK_OP_RAMP 2  /* phase exp(i*pi*s*F) with F = (idx >> qubit) & (2^nbits-1), predicated */
+#define SK_OP_QFT 3   /* QFT layers on bits [qubit, qubit+nbits) of the window [m[0], m[1]] (each H(j)
+                       * then its CP fan from all lower bits), FFT form; m[2] = previous chunk's top bit */
 
 typedef struct {
   int32_t kind;

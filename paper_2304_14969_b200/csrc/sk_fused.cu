@@ -37,8 +37,9 @@ constexpr int kMaxS = SK_MAX_STAGES;
 constexpr int kMaxR = SK_MAX_REG_BITS;
 constexpr int kMaxRuns = 16;
 
-enum KKind : int { K_MAT = 0, K_MATR = 1, K_PHASE = 2, K_TPHASE = 3, K_BFLY = 4 };
-enum KFlag : unsigned { F_TPRED = 1, F_QMASK = 2, F_C0REAL = 4, F_FOLD = 8, F_TABLE = 16, F_C0ONE = 32 };
+enum KKind : int { K_MAT = 0, K_MATR = 1, K_PHASE = 2, K_TPHASE = 3, K_BFLY = 4, K_QFTS = 5 };
+enum KFlag : unsigned { F_TPRED = 1, F_QMASK = 2, F_C0REAL = 4, F_FOLD = 8, F_TABLE = 16, F_C0ONE = 32,
+                        F_ENTRY = 64, F_END = 128, F_SCALE = 256 };
 
 struct Run {  // bits [src, src+w) of a counter go to bits [dst, dst+w)
   uint8_t src, dst, w, pad;
@@ -56,6 +57,7 @@ struct DStage {
 struct DSweep {
   int ntile;
   int nstages;
+  int qft_only;  // every kernel op is a K_QFTS chunk: use the specialised kernel
   int nb;
   Run brun[kMaxRuns];  // tile index (blockIdx) bits -> non-tile global bits
   DStage st[kMaxS];
@@ -245,11 +247,165 @@ __device__ __forceinline__ bool phase_dispatch(int pat, vec2_t<R> (&a)[1 << NR],
     default: break;                                 \
   }
 
+// ---------------------------------------------------------------------------
+// QFT window chunk in FFT form (K_QFTS).  For a window of QFT layers
+// j = w_hi..w_lo (each H(j) followed by its CP fan from all lower bits), a
+// chunk of L consecutive layer bits held in register slots TOP-L+1..TOP:
+//  * entry (not the first chunk): per-element phase
+//      exp(i pi [Th_all * sum_{i in chunk} e_i 2^i + Th_new * Lv])
+//    Th_all = sum_{j in earlier chunks} b_j 2^-j (their CPs onto this chunk),
+//    Th_new = the same over the previous chunk only (its deferred below-window
+//    phase), Lv = index bits below the window; in 2^-64-turn fixed point
+//    Th = brev64(bits) exactly;
+//  * L butterflies y0 = a0 + a1, y1 = (a0 - a1) exp(i pi sum_{p<P} e_p 2^(p-P))
+//    with compile-time internal twiddles (the 1/sqrt2 per layer is deferred);
+//  * end (last chunk, w_lo > 0): phase exp(i pi Lv sum_{i in chunk} e_i 2^-i)
+//    (the chunk's deferred below-window phase); the window's (1/sqrt2)^K
+//    scale rides on the last chunk's first phase.
+// All deferred factors are diagonal in bits no later butterfly of the window
+// touches, so moving them is exact (checked against the oracle by
+// tests/test_kernel_lowering.py and tests/test_executor_gpu.py).
+// ---------------------------------------------------------------------------
+template <typename R>
+__device__ __forceinline__ vec2_t<R> turn_phase(uint64_t t) {
+  if (sizeof(R) == 4) {
+    const float ang = (float)(int32_t)(uint32_t)(t >> 32) * 1.4629180792671596e-09f;
+    float fs, fc;
+    __sincosf(ang, &fs, &fc);
+    return mk<R>((R)fc, (R)fs);
+  } else {
+    double ds, dc;
+    sincospi((double)(int64_t)t * 1.0842021724855044e-19, &ds, &dc);
+    return mk<R>((R)dc, (R)ds);
+  }
+}
+
+// multiply by exp(i pi K / 8), K compile-time
+template <typename R, int K>
+__device__ __forceinline__ vec2_t<R> mul_pi8(vec2_t<R> x) {
+  constexpr R c1 = (R)0.92387953251128674, s1 = (R)0.38268343236508978, h = (R)0.70710678118654752;
+  if constexpr (K == 0) return x;
+  else if constexpr (K == 4) return mk<R>(-x.y, x.x);
+  else if constexpr (K == 2) return mk<R>(h * (x.x - x.y), h * (x.x + x.y));
+  else if constexpr (K == 6) return mk<R>(-h * (x.x + x.y), h * (x.x - x.y));
+  else {
+    constexpr R cr = K == 1 ? c1 : K == 3 ? s1 : K == 5 ? -s1 : -c1;
+    constexpr R ci = K == 1 ? s1 : K == 3 ? c1 : K == 5 ? c1 : s1;
+    return mk<R>(cr * x.x - ci * x.y, cr * x.y + ci * x.x);
+  }
+}
+
+template <int NR, int L, int TOP, int P, int E>
+__host__ __device__ constexpr int qft_k8() {  // internal twiddle of pair base E at layer slot P, units of pi/8
+  int k = 0;
+  for (int p = TOP - L + 1; p < P; ++p)
+    if ((E >> p) & 1) k += 1 << (3 - (P - p));
+  return k;
+}
+
+template <typename R, int NR, int L, int TOP, int P, int E>
+__device__ __forceinline__ void qft_pair(vec2_t<R> (&a)[1 << NR]) {
+  if constexpr (E < (1 << NR)) {
+    if constexpr (!((E >> P) & 1)) {
+      constexpr int E1 = E | (1 << P);
+      const vec2_t<R> s = mk<R>(a[E].x + a[E1].x, a[E].y + a[E1].y);
+      const vec2_t<R> d = mk<R>(a[E].x - a[E1].x, a[E].y - a[E1].y);
+      a[E] = s;
+      a[E1] = mul_pi8<R, qft_k8<NR, L, TOP, P, E>()>(d);
+    }
+    qft_pair<R, NR, L, TOP, P, E + 1>(a);
+  }
+}
+
+template <typename R, int NR, int L, int TOP, int P>
+__device__ __forceinline__ void qft_layers(vec2_t<R> (&a)[1 << NR]) {
+  if constexpr (P >= TOP - L + 1 && P >= 0) {
+    qft_pair<R, NR, L, TOP, P, 0>(a);
+    qft_layers<R, NR, L, TOP, P - 1>(a);
+  }
+}
+
+// a[e] *= phase(base + sum_{layer slots p} e_p u_p) * scale, walked in Gray
+// order (one complex multiply per element and per layer-bit flip)
+template <typename R, int NR, int L, int TOP>
+__device__ __forceinline__ void qft_phase(vec2_t<R> (&a)[1 << NR], uint64_t base, const uint64_t (&ut)[NR], R scale) {
+  vec2_t<R> u[NR];
+#pragma unroll
+  for (int p = 0; p < NR; ++p)
+    if (p >= TOP - L + 1 && p <= TOP) u[p] = turn_phase<R>(ut[p]);
+  vec2_t<R> w = turn_phase<R>(base);
+  w = mk<R>(w.x * scale, w.y * scale);
+  a[0] = cmul<R>(a[0], w);
+#pragma unroll
+  for (int k = 1; k < (1 << NR); ++k) {
+    const int b = ctz_c(k);
+    const int e = k ^ (k >> 1);
+    if (b >= TOP - L + 1 && b <= TOP) {
+      if ((e >> b) & 1)
+        w = cmul<R>(w, u[b]);
+      else
+        w = mk<R>(w.x * u[b].x + w.y * u[b].y, w.y * u[b].x - w.x * u[b].y);
+    }
+    a[e] = cmul<R>(a[e], w);
+  }
+}
+
+template <typename R, int NR, int L, int TOP>
+__device__ __forceinline__ void qft_chunk(const KOp<R>* __restrict__ op, const KHdr& h, vec2_t<R> (&a)[1 << NR],
+                                          uint64_t gthr) {
+  if constexpr (L >= 1 && L <= NR && TOP < NR && TOP - L + 1 >= 0) {
+    const unsigned fl = h.flags;
+    const R scale = op->m[0];
+    bool scaled = !(fl & F_SCALE);
+    const uint64_t lv = gthr & op->qmask;
+    if (fl & F_ENTRY) {
+      const uint64_t th_all = __brevll(gthr & op->tmask), th_new = __brevll(gthr & op->tval);
+      uint64_t ut[NR];
+#pragma unroll
+      for (int p = 0; p < NR; ++p) ut[p] = th_all << ((h.lo + p - (TOP - L + 1)) & 63);
+      const bool here = !scaled && !(fl & F_END);
+      qft_phase<R, NR, L, TOP>(a, th_new * lv, ut, here ? scale : (R)1);
+      scaled = scaled || here;
+    }
+    qft_layers<R, NR, L, TOP, TOP>(a);
+    if (fl & F_END) {
+      uint64_t ut[NR];
+#pragma unroll
+      for (int p = 0; p < NR; ++p) ut[p] = lv << ((63 - (h.lo + p - (TOP - L + 1))) & 63);
+      qft_phase<R, NR, L, TOP>(a, 0, ut, scaled ? (R)1 : scale);
+      scaled = true;
+    }
+    if (!scaled) {
+#pragma unroll
+      for (int e = 0; e < (1 << NR); ++e) a[e] = mk<R>(a[e].x * scale, a[e].y * scale);
+    }
+  }
+}
+
+template <typename R, int NR>
+__device__ __forceinline__ void qft_dispatch(const KOp<R>* __restrict__ op, const KHdr& h, vec2_t<R> (&a)[1 << NR],
+                                             uint64_t gthr) {
+  switch (h.nbits * 8 + h.slot) {
+#define SK_Q(L, TOP) \
+  case L * 8 + TOP: qft_chunk<R, NR, L, TOP>(op, h, a, gthr); break;
+    SK_Q(1, 0) SK_Q(1, 1) SK_Q(1, 2) SK_Q(1, 3)
+    SK_Q(2, 1) SK_Q(2, 2) SK_Q(2, 3)
+    SK_Q(3, 2) SK_Q(3, 3)
+    SK_Q(4, 3)
+#undef SK_Q
+    default: break;
+  }
+}
+
 template <typename R, int NR>
 __device__ __forceinline__ void apply_kop(const KOp<R>* __restrict__ op, vec2_t<R> (&a)[1 << NR], uint64_t gthr) {
   const uint4 raw = *reinterpret_cast<const uint4*>(&op->h);
   KHdr h;
   memcpy(&h, &raw, sizeof(h));
+  if (h.kind == K_QFTS) {
+    qft_dispatch<R, NR>(op, h, a, gthr);
+    return;
+  }
   if ((h.flags & F_TPRED) && (gthr & op->tmask) != op->tval) return;
   const uint32_t emask = h.emask;
   const int kind = h.kind;
@@ -302,7 +458,7 @@ __device__ __forceinline__ void apply_kop(const KOp<R>* __restrict__ op, vec2_t<
   }
 }
 
-template <typename R, int NR>
+template <typename R, int NR, bool QFTONLY>
 __global__ void __launch_bounds__(512, 2) k_sweep(vec2_t<R>* __restrict__ amps, const __grid_constant__ DSweep sw,
                                                   const KOp<R>* __restrict__ ops) {
   using V = vec2_t<R>;
@@ -338,7 +494,16 @@ __global__ void __launch_bounds__(512, 2) k_sweep(vec2_t<R>* __restrict__ amps, 
         a[e] = *reinterpret_cast<const V*>(smraw + so);
       }
     }
-    for (int o = st.op_begin; o < st.op_end; ++o) apply_kop<R, NR>(ops + o, a, gthr);
+    if (QFTONLY) {
+      for (int o = st.op_begin; o < st.op_end; ++o) {
+        const uint4 raw = *reinterpret_cast<const uint4*>(&ops[o].h);
+        KHdr h;
+        memcpy(&h, &raw, sizeof(h));
+        qft_dispatch<R, NR>(ops + o, h, a, gthr);
+      }
+    } else {
+      for (int o = st.op_begin; o < st.op_end; ++o) apply_kop<R, NR>(ops + o, a, gthr);
+    }
     if (s == ns - 1) {
       char* p = reinterpret_cast<char*>(amps + gthr);
 #pragma unroll
@@ -604,6 +769,39 @@ static int lower_op(const StageCtx& c, const sk_op& op, int o, int width, std::v
     }
     return SK_OK;
   }
+  if (op.kind == SK_OP_QFT) {
+    const int c_lo = op.qubit, L = op.nbits, c_hi = c_lo + L - 1;
+    const int w_lo = (int)op.m[0], w_hi = (int)op.m[1], prev_hi = (int)op.m[2];
+    if (L < 1 || L > c.NR || c_lo < w_lo || c_hi > w_hi || w_lo < 0 || w_hi >= width || w_hi - w_lo > 62)
+      return set_error(SK_EVALUE, "op %d: bad QFT chunk [%d, %d]", o, c_lo, c_hi);
+    const int s0 = c.slot_of[c_lo];
+    for (int b = c_lo; b <= c_hi; ++b)
+      if (s0 < 0 || c.slot_of[b] != s0 + (b - c_lo))
+        return set_error(SK_EVALUE, "op %d: QFT chunk bit %d not in consecutive register slots", o, b);
+    const bool entry = c_hi < w_hi, end = c_lo == w_lo && w_lo > 0;
+    if (entry && (prev_hi <= c_hi || prev_hi > w_hi)) return set_error(SK_EVALUE, "op %d: bad previous chunk", o);
+    for (int p = 0; p < c.NR; ++p) {
+      const int q = __builtin_ctzll(c.reg_off[p]);
+      if (entry && q > c_hi && q <= w_hi)
+        return set_error(SK_EVALUE, "op %d: earlier window bit %d held in a register", o, q);
+      if ((entry || end) && q < w_lo) return set_error(SK_EVALUE, "op %d: below-window bit %d in a register", o, q);
+    }
+    auto range = [](int lo, int hi) -> uint64_t {
+      return hi < lo ? 0ull : (((hi - lo + 1) >= 64 ? ~0ull : ((1ull << (hi - lo + 1)) - 1)) << lo);
+    };
+    HostKOp k;
+    k.kind = K_QFTS;
+    k.slot = s0 + L - 1;
+    k.lo = c_lo;
+    k.nbits = L;
+    k.flags = (entry ? F_ENTRY : 0u) | (end ? F_END : 0u) | (c_lo == w_lo ? F_SCALE : 0u);
+    k.tmask = range(c_hi + 1, w_hi);
+    k.tval = entry ? range(c_hi + 1, prev_hi) : 0;
+    k.qmask = range(0, w_lo - 1);
+    k.m[0] = std::pow(0.5, 0.5 * (w_hi - w_lo + 1));
+    out.push_back(k);
+    return SK_OK;
+  }
   return set_error(SK_EVALUE, "op %d: unknown kind %d", o, op.kind);
 }
 
@@ -650,7 +848,8 @@ template <typename R, int NR>
 static int launch_sweeps(sk_state* s, const sk_program* p, int first, int count, DevCtx* c) {
   static bool attr_set[64] = {false};
   if (!attr_set[s->device]) {
-    SK_CUDA(cudaFuncSetAttribute(k_sweep<R, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    SK_CUDA(cudaFuncSetAttribute(k_sweep<R, NR, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    SK_CUDA(cudaFuncSetAttribute(k_sweep<R, NR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     attr_set[s->device] = true;
   }
   for (int i = first; i < first + count; ++i) {
@@ -660,7 +859,10 @@ static int launch_sweeps(sk_state* s, const sk_program* p, int first, int count,
     const unsigned threads = 1u << (T - NR);
     const size_t smem = ((size_t)1 << T) * sizeof(vec2_t<R>);
     if (tiles > 0x7fffffffull) return set_error(SK_EVALUE, "too many tiles (%d bits outside the tile)", s->width - T);
-    k_sweep<R, NR><<<(unsigned)tiles, threads, smem, c->stream>>>((vec2_t<R>*)s->d, d, (const KOp<R>*)p->d_ops);
+    if (d.qft_only)
+      k_sweep<R, NR, true><<<(unsigned)tiles, threads, smem, c->stream>>>((vec2_t<R>*)s->d, d, (const KOp<R>*)p->d_ops);
+    else
+      k_sweep<R, NR, false><<<(unsigned)tiles, threads, smem, c->stream>>>((vec2_t<R>*)s->d, d, (const KOp<R>*)p->d_ops);
     SK_CHECK_LAUNCH();
   }
   return SK_OK;
@@ -743,6 +945,10 @@ static int lower_program(int width, int dtype, const sk_sweep* sweeps, int nswee
       }
       st.op_end = (int)kops.size();
     }
+    d.qft_only = 1;
+    for (int s2 = 0; s2 < d.nstages; ++s2)
+      for (int o2 = d.st[s2].op_begin; o2 < d.st[s2].op_end; ++o2)
+        if (kops[o2].kind != K_QFTS) d.qft_only = 0;
     dsw.push_back(d);
   }
   return SK_OK;

@@ -80,8 +80,17 @@ def _run_segment(gates, width, state: DenseKet, phys: list[int], dtype: str, dev
         return phys
     ops, phys = fusion.lower(Circuit(width, tuple(gates)), phys)
     ops = fusion.fuse_diagonal_runs(ops)
-    if ops:
-        Program(fusion.plan_ops(ops, width, dtype, phys=phys), device).run(state)
+    if not ops:
+        return phys
+    plan = None
+    if fusion.match_qft(ops, width):  # the QFT body: FFT-form windows
+        try:
+            plan = fusion.plan_qft(width, dtype, phys=phys)
+        except ValueError:
+            plan = None
+    if plan is None:
+        plan = fusion.plan_ops(ops, width, dtype, phys=phys)
+    Program(plan, device).run(state)
     return phys
 
 

@@ -35,7 +35,7 @@ import numpy as np
 from . import _lib
 from .circuit import Circuit, gate_matrix
 
-MAT, DIAG, RAMP = _lib.SK_OP_MAT, _lib.SK_OP_DIAG, _lib.SK_OP_RAMP
+MAT, DIAG, RAMP, QFT = _lib.SK_OP_MAT, _lib.SK_OP_DIAG, _lib.SK_OP_RAMP, _lib.SK_OP_QFT
 MAX_STAGES = _lib.SK_MAX_STAGES
 
 # kernel geometry per dtype (csrc/sk_fused.cu): register bits, max tile bits,
@@ -56,6 +56,8 @@ class Op:
     @property
     def tmask(self) -> int:
         """Bits acted on non-diagonally."""
+        if self.kind == QFT:
+            return ((1 << self.nbits) - 1) << self.qubit
         return (1 << self.qubit) if self.kind == MAT else 0
 
     @property
@@ -63,6 +65,8 @@ class Op:
         """Every bit the op reads or acts on."""
         if self.kind == RAMP:
             s = ((1 << self.nbits) - 1) << self.qubit
+        elif self.kind == QFT:  # reads the window above and everything below it
+            s = (1 << (int(self.m[1]) + 1)) - 1
         else:
             s = 1 << self.qubit
         return s | self.ctrl_mask
@@ -297,11 +301,113 @@ def plan_ops(ops: list[Op], width: int, dtype: str = "c64", tile_bits: int | Non
                 n_gates, len(ops))
 
 
+_H_M8 = _m8(gate_matrix("h"))
+
+
+def match_qft(ops: list[Op], n: int) -> bool:
+    """True when `ops` is exactly the n-qubit QFT body (build_qft without the
+    final swaps): for j = n-1..0, H(j) then the fan of CP(pi/2^k) from j-k
+    onto j (a RAMP over bits [0, j) with s = 2^-j; j = 1 is a single CP)."""
+    i = 0
+    for j in range(n - 1, -1, -1):
+        if i >= len(ops):
+            return False
+        op = ops[i]
+        if op.kind != MAT or op.qubit != j or op.ctrl_mask or max(abs(a - b) for a, b in zip(op.m, _H_M8)) > 0:
+            return False
+        i += 1
+        if j >= 2:
+            if i >= len(ops):
+                return False
+            r = ops[i]
+            if (r.kind != RAMP or r.qubit != 0 or r.nbits != j or r.ctrl_mask != 1 << j or r.ctrl_val != 1 << j
+                    or abs(r.m[0] - 2.0 ** -j) > 1e-13 * 2.0 ** -j):
+                return False
+            i += 1
+        elif j == 1:
+            if i >= len(ops):
+                return False
+            d = ops[i]
+            want = (1.0, 0.0, 0.0, 0.0, 0.0, 0.0, math.cos(math.pi / 2), math.sin(math.pi / 2))
+            if (d.kind != DIAG or d.qubit != 1 or d.ctrl_mask != 1 or d.ctrl_val != 1
+                    or max(abs(a - b) for a, b in zip(d.m, want)) > 1e-15):
+                return False
+            i += 1
+    return i == len(ops)
+
+
+def plan_qft(n: int, dtype: str = "c64", tile_bits: int | None = None, low_bits: int | None = None,
+             phys=None, n_gates: int = 0) -> Plan:
+    """Sweeps for the QFT body in FFT form: windows of target bits from the
+    top (each at most T - low bits, the bottom window up to T bits), each
+    window split into register chunks of NR bits; one QFT op per chunk."""
+    geo = GEOMETRY[dtype]
+    nreg = geo["nreg"]
+    T = min(tile_bits or geo["tile"], n)
+    low = min(low_bits if low_bits is not None else geo["low"], T)
+    windows = []
+    hi = n - 1
+    while hi >= 0:
+        if hi + 1 <= T:  # bottom window: everything left fits one tile
+            windows.append((0, hi))
+            break
+        k = T - low
+        windows.append((hi - k + 1, hi))
+        hi -= k
+    sweeps = []
+    for w_lo, w_hi in windows:
+        tile_mask = ((1 << low) - 1) | (((1 << (w_hi - w_lo + 1)) - 1) << w_lo)
+        b = 0
+        while bin(tile_mask).count("1") < T:
+            tile_mask |= 1 << b
+            b += 1
+        tile = _bits(tile_mask)
+        stages = []
+        K = w_hi - w_lo + 1
+        sizes = [K % nreg or nreg] + [nreg] * ((K - (K % nreg or nreg)) // nreg)  # short chunk first
+        c_hi = w_hi
+        prev_hi = None
+        for ci, size in enumerate(sizes):
+            c_lo = c_hi - size + 1
+            last = ci == len(sizes) - 1
+            # pad bits must not be read by this chunk's phases: no earlier-chunk window
+            # bits (entry twiddle) and no below-window bits when a twiddle reads L
+            uses_l = (ci > 0) or (last and w_lo > 0)
+            allowed = [x for x in sorted(tile, reverse=True)
+                       if not (c_lo <= x <= w_hi) and not (uses_l and x < w_lo)]
+            regs = list(range(c_lo, c_hi + 1))
+            for pref in (lambda x: x >= low, lambda x: True):
+                for x in allowed:
+                    if len(regs) < nreg and x not in regs and pref(x):
+                        regs.append(x)
+            if len(regs) < nreg:
+                raise ValueError("QFT window chunk cannot be padded")
+            op = Op(QFT, c_lo, (float(w_lo), float(w_hi), float(prev_hi if prev_hi is not None else -1),
+                                0, 0, 0, 0, 0), nbits=size)
+            stages.append(StagePlan(sorted(regs), [op]))
+            prev_hi = c_hi
+            c_hi = c_lo - 1
+        low_mask = (1 << low) - 1
+        if len(tile) - nreg >= low and any((1 << x) & low_mask for x in stages[-1].reg_bits):
+            stages.append(StagePlan(sorted(tile, reverse=True)[:nreg], []))  # store stage: lanes on low bits
+        if len(stages) > MAX_STAGES:
+            raise ValueError("QFT window needs too many stages")
+        sweeps.append(SweepPlan(tile, stages))
+    return Plan(n, dtype, nreg, sweeps, list(phys) if phys is not None else list(range(n)), n_gates,
+                sum(len(st.ops) for sp in sweeps for st in sp.stages))
+
+
 def plan_circuit(circuit: Circuit, dtype: str = "c64", tile_bits: int | None = None,
-                 low_bits: int | None = None, fuse: bool = True) -> Plan:
+                 low_bits: int | None = None, fuse: bool = True, qft: bool = True) -> Plan:
     ops, phys = lower(circuit)
     if fuse:
         ops = fuse_diagonal_runs(ops)
+    geo = GEOMETRY[dtype]
+    if qft and fuse and circuit.width >= geo["nreg"] + 1 and match_qft(ops, circuit.width):
+        try:
+            return plan_qft(circuit.width, dtype, tile_bits, low_bits, phys, len(circuit.gates))
+        except ValueError:
+            pass  # geometry the QFT form cannot pad: fall back to generic sweeps
     return plan_ops(ops, circuit.width, dtype, tile_bits, low_bits, phys, len(circuit.gates))
 
 
@@ -342,6 +448,28 @@ def to_c(plan: Plan):
 def apply_op_numpy(amps: np.ndarray, op: Op) -> None:
     n = amps.size
     idx = np.arange(n, dtype=np.int64)
+    if op.kind == QFT:  # one register chunk of a QFT window, FFT form (see csrc/sk_fused.cu)
+        w_lo, w_hi, prev_hi = int(op.m[0]), int(op.m[1]), int(op.m[2])
+        c_lo, c_hi = op.qubit, op.qubit + op.nbits - 1
+        bit = lambda q: (idx >> q) & 1  # noqa: E731
+        L = idx & ((1 << w_lo) - 1)
+        if c_hi < w_hi:  # entry: cross phases with earlier chunks + their deferred below-window phase
+            th_all = sum(bit(j) * 2.0 ** -j for j in range(c_hi + 1, w_hi + 1))
+            th_new = sum(bit(j) * 2.0 ** -j for j in range(c_hi + 1, prev_hi + 1))
+            cur = sum(bit(i) << i for i in range(c_lo, c_hi + 1))
+            amps *= np.exp(1j * np.pi * np.mod(th_all * cur + th_new * L, 2.0))
+        h = 1 / math.sqrt(2)
+        for j in range(c_hi, c_lo - 1, -1):
+            i0 = idx[bit(j) == 0]
+            i1 = i0 | (1 << j)
+            a0, a1 = amps[i0].copy(), amps[i1].copy()
+            amps[i0] = h * (a0 + a1)
+            amps[i1] = h * (a0 - a1)
+            inner = sum(bit(i) * 2.0 ** (i - j) for i in range(c_lo, j))
+            amps *= np.where(bit(j) == 1, np.exp(1j * np.pi * inner), 1.0)
+        if c_lo == w_lo and w_lo > 0:  # window end: this chunk's deferred below-window phase
+            amps *= np.exp(1j * np.pi * np.mod(L * sum(bit(i) * 2.0 ** -i for i in range(c_lo, c_hi + 1)), 2.0))
+        return
     sel = (idx & op.ctrl_mask) == op.ctrl_val
     if op.kind == MAT:
         bit = 1 << op.qubit
@@ -368,5 +496,7 @@ def run_plan_numpy(plan: Plan, amps: np.ndarray) -> np.ndarray:
             for op in st.ops:
                 if op.kind == MAT:
                     assert op.qubit in st.reg_bits and op.qubit in sp.tile_bits
+                if op.kind == QFT:
+                    assert set(range(op.qubit, op.qubit + op.nbits)) <= set(st.reg_bits)
                 apply_op_numpy(amps, op)
     return amps

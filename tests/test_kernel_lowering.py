@@ -17,8 +17,9 @@ from paper_2304_14969_b200.circuit import (Circuit, Gate, build_qft, build_rando
 
 from conftest import random_state
 
-K_MAT, K_MATR, K_PHASE, K_TPHASE, K_BFLY = range(5)
+K_MAT, K_MATR, K_PHASE, K_TPHASE, K_BFLY, K_QFTS = range(6)
 F_TPRED, F_QMASK, F_C0REAL, F_FOLD, F_TABLE, F_C0ONE = 1, 2, 4, 8, 16, 32
+F_ENTRY, F_END, F_SCALE = 64, 128, 256
 NS = _lib.SK_MAX_STAGES + 1
 
 
@@ -43,6 +44,52 @@ def tau(turn, gthr, lo, fmask):
     return np.exp(2j * np.pi * (t.astype(np.float64) / 2.0 ** 64))
 
 
+def brev64(x):
+    out = np.zeros_like(x)
+    for b in range(64):
+        out |= ((x >> np.uint64(b)) & np.uint64(1)) << np.uint64(63 - b)
+    return out
+
+
+def turn_phase(t):
+    return np.exp(2j * np.pi * (t.astype(np.float64) / 2.0 ** 64))
+
+
+def qft_chunk(amps, g, gthr, regs, e_of, slot, lo, nbits, flags, tmask, tval, qmask, scale):
+    """K_QFTS exactly as the kernel computes it (wrapping uint64 turns)."""
+    u64 = lambda v: np.uint64(v & (2**64 - 1))  # noqa: E731
+    top, L = slot, nbits
+    layer_slots = range(top - L + 1, top + 1)
+    lv = gthr & u64(qmask)
+    scaled = not (flags & F_SCALE)
+    if flags & F_ENTRY:
+        th_all, th_new = brev64(gthr & u64(tmask)), brev64(gthr & u64(tval))
+        t = th_new * lv
+        for p in layer_slots:
+            t = t + np.where((e_of >> p) & 1, th_all << u64(lo + p - (top - L + 1)), np.uint64(0)).astype(np.uint64)
+        here = not scaled and not (flags & F_END)
+        amps *= turn_phase(t) * (scale if here else 1.0)
+        scaled = scaled or here
+    for P in range(top, top - L, -1):
+        q = regs[P]
+        i0 = np.nonzero(((g >> np.uint64(q)) & np.uint64(1)) == 0)[0]
+        i1 = i0 | (1 << q)
+        a0, a1 = amps[i0].copy(), amps[i1].copy()
+        k8 = np.zeros(i0.size, dtype=np.int64)
+        for p in range(top - L + 1, P):
+            k8 += ((e_of[i0] >> p) & 1) << (3 - (P - p))
+        amps[i0] = a0 + a1
+        amps[i1] = (a0 - a1) * np.exp(1j * np.pi * k8 / 8)
+    if flags & F_END:
+        t = np.zeros_like(gthr)
+        for p in layer_slots:
+            t = t + np.where((e_of >> p) & 1, lv << u64(63 - (lo + p - (top - L + 1))), np.uint64(0)).astype(np.uint64)
+        amps *= turn_phase(t) * (1.0 if scaled else scale)
+        scaled = True
+    if not scaled:
+        amps *= scale
+
+
 def emulate(plan: fusion.Plan, amps: np.ndarray) -> np.ndarray:
     I, Rl, stage_ops = lower(plan)
     n = plan.width
@@ -58,6 +105,9 @@ def emulate(plan: fusion.Plan, amps: np.ndarray) -> np.ndarray:
             for k in range(stage_ops[si, st], stage_ops[si, st + 1]):
                 kind, slot, pat, emask, flags, lo, nbits, tmask, tval, qmask, turn, fmask = (int(v) for v in I[k])
                 m = Rl[k]
+                if kind == K_QFTS:
+                    qft_chunk(amps, g, gthr, regs, e_of, slot, lo, nbits, flags, tmask, tval, qmask, m[0])
+                    continue
                 ok = np.ones(1 << n, dtype=bool)
                 if flags & F_TPRED:
                     ok = (gthr & np.uint64(tmask & (2**64 - 1))) == np.uint64(tval & (2**64 - 1))
@@ -103,13 +153,28 @@ def emulate(plan: fusion.Plan, amps: np.ndarray) -> np.ndarray:
 @pytest.mark.parametrize("n", [5, 9, 14])
 def test_qft_lowering(rng, dtype, n):
     x = random_state(n, rng)
-    plan = fusion.plan_circuit(build_qft(n), dtype=dtype, tile_bits=min(n, 8), low_bits=min(3, n - 4))
+    plan = fusion.plan_circuit(build_qft(n), dtype=dtype, tile_bits=min(n, 8), low_bits=min(3, n - 4), qft=False)
+    got = emulate(plan, x.copy())
+    assert np.max(np.abs(got - O.dft_oracle(x))) < 1e-12
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("n,tile,low", [(9, 7, 2), (12, 8, 3), (14, 10, 4), (15, 13, 5)])
+def test_qft_fft_form_lowering(rng, dtype, n, tile, low):
+    """The QFT-window (FFT-form) kernel path: chunk ops, fixed-point entry and
+    end twiddles, compile-time internal twiddles, deferred scale."""
+    x = random_state(n, rng)
+    t = min(tile, fusion.GEOMETRY[dtype]["tile"])
+    plan = fusion.plan_circuit(build_qft(n), dtype=dtype, tile_bits=t, low_bits=low)
+    assert all(op.kind == fusion.QFT for sp in plan.sweeps for st in sp.stages for op in st.ops)
+    I, _, _ = lower(plan)
+    assert set(int(v) for v in I[:, 0]) == {K_QFTS}
     got = emulate(plan, x.copy())
     assert np.max(np.abs(got - O.dft_oracle(x))) < 1e-12
 
 
 def test_qft_lowering_uses_butterflies_and_folds():
-    plan = fusion.plan_circuit(build_qft(16), dtype="c64")
+    plan = fusion.plan_circuit(build_qft(16), dtype="c64", qft=False)
     I, _, _ = lower(plan)
     kinds = list(I[:, 0])
     assert kinds.count(K_BFLY) == 16
