@@ -40,7 +40,10 @@ MAX_STAGES = _lib.SK_MAX_STAGES
 
 # kernel geometry per dtype (csrc/sk_fused.cu): register bits, max tile bits,
 # low contiguous bits (256 B per warp access)
-GEOMETRY = {"c64": dict(nreg=4, tile=13, low=5), "c128": dict(nreg=3, tile=12, low=4)}
+GEOMETRY = {"c64": dict(nreg=4, tile=13, low=5, qft_tile=12, qft_low=4),
+            "c128": dict(nreg=3, tile=12, low=4, qft_tile=10, qft_low=4)}
+# QFT windows use smaller tiles (more CTAs per SM; measured best on B200 by
+# scripts/tune_qft.py: c64 QFT-27 1.57 ms at T=12/low=4 vs 1.74 ms at T=13/low=5)
 
 
 @dataclass
@@ -343,8 +346,8 @@ def plan_qft(n: int, dtype: str = "c64", tile_bits: int | None = None, low_bits:
     window split into register chunks of NR bits; one QFT op per chunk."""
     geo = GEOMETRY[dtype]
     nreg = geo["nreg"]
-    T = min(tile_bits or geo["tile"], n)
-    low = min(low_bits if low_bits is not None else geo["low"], T)
+    T = min(tile_bits or geo["qft_tile"], n)
+    low = min(low_bits if low_bits is not None else geo["qft_low"], T)
     windows = []
     hi = n - 1
     while hi >= 0:
