@@ -1,13 +1,17 @@
 """Benchmark: exact QFT on 27 qubits (BASELINE.json configs[1]) on B200.
 
-Metric (BASELINE.json "QFT sec & HBM GB/s"): QFT gate-layers per second
-(one layer = H(j) plus its controlled-phase fan), whole job over all ranks;
-the line also carries the QFT seconds and the HBM GB/s of the fused sweeps.
+Metric (BASELINE.json "QFT sec & HBM GB/s"): QFT amplitude-layer updates
+per second = (QFT layers x amplitudes) / time, whole job over all ranks (one
+layer = H(j) plus its controlled-phase fan; work-normalised so weak scaling
+reads directly); the line also carries the QFT seconds, the gate-layers/s
+and the HBM GB/s of the fused sweeps.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-A step is one full QFT-27 (fp32 amplitudes, 1 GiB, random normalised input,
-SWAPs as label permutations like the reference engine) on a resident state.
+A step is one full QFT-27 at N=1 (fp32 amplitudes, 1 GiB, random normalised
+input, SWAPs as label permutations like the reference engine) on a resident
+state; at N GPUs one QFT-(27+log2 N) sharded by global qubits (1 GiB per GPU,
+two NCCL all-to-alls per QFT).
 `e2e` repeats it through the public C-ABI entry points with host buffers:
 pinned host state -> device, QFT, device -> host, copies inside the timing.
 `--impl reference` times the reference's CPU path (the oracle port of its
@@ -30,10 +34,6 @@ sys.path.insert(0, str(ROOT))
 
 N_QUBITS = 27
 CPP_CORES = 1  # the reference's NumPy ufuncs are single-threaded
-
-
-def qft_layers(n: int) -> int:
-    return n
 
 
 # ---------------------------------------------------------------------------
@@ -65,7 +65,7 @@ def cpu_layer_sample(n: int, n_cp: int | None = None):
 def cpu_baseline(n: int):
     t_h, t_cp = cpu_layer_sample(n, 4)
     t_qft = n * t_h + (n * (n - 1) // 2) * t_cp
-    return {"value": qft_layers(n) / t_qft, "unit": "gate-layers/s", "cores": CPP_CORES, "kind": "port",
+    return {"value": n * float(1 << n) / t_qft, "unit": "amp-layers/s", "cores": CPP_CORES, "kind": "port",
             "qft_sec": t_qft,
             "sample": f"1 H + 4 CP kernels of QFT-{n} on a 2^{n} complex128 state via the oracle port of the "
                       f"reference's NumPy kernels (ket.py:133-164), 1 thread; extrapolated to the QFT-{n} mix "
@@ -82,18 +82,18 @@ def run_reference(args, rank: int, world: int):
         if i >= args.warmup:
             times.append(t_h + ((n - 1) // 2) * t_cp)
     t = statistics.mean(times)
-    value = 1.0 / t
-    line = {"metric": f"QFT-{n} gate-layers/s", "value": value, "unit": "gate-layers/s", "n_gpus": world,
+    value = float(1 << n) / t  # one layer over 2^n amplitudes per step
+    line = {"metric": "QFT amplitude-layer updates/s", "value": value, "unit": "amp-layers/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": f"exact QFT on {n} qubits (BASELINE configs[1]); reference CPU path",
                        "qubits": n, "step": f"one average QFT-{n} layer: 1 H + {(n - 1) // 2} CP kernels"},
             "qft_sec": n * t,
-            "cpu_baseline": {"value": value, "unit": "gate-layers/s", "cores": CPP_CORES, "kind": "port",
+            "cpu_baseline": {"value": value, "unit": "amp-layers/s", "cores": CPP_CORES, "kind": "port",
                              "sample": f"each step = 1 H + {(n - 1) // 2} CP kernels at width {n}, complex128, "
                                        f"oracle port of ket.py:133-164 (NumPy, single-threaded)"},
-            "e2e": {"value": value, "unit": "gate-layers/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": value, "unit": "amp-layers/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
@@ -149,13 +149,11 @@ class ClockSampler:
 # our arm
 # ---------------------------------------------------------------------------
 def run_ours(args, rank: int, world: int):
-    import numpy as np
     import torch
 
     from paper_2304_14969_b200 import _lib
-    from paper_2304_14969_b200.circuit import build_qft
-    from paper_2304_14969_b200.executor import compile_circuit
-    from paper_2304_14969_b200.ket import DenseKet, set_default_device
+    from paper_2304_14969_b200.distributed import ShardedQFT
+    from paper_2304_14969_b200.ket import set_default_device
 
     dev = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(dev)
@@ -164,24 +162,40 @@ def run_ours(args, rank: int, world: int):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
-    stream = torch.cuda.Stream(device=dev)  # one stream: library kernels and the timing events
+    stream = torch.cuda.Stream(device=dev)  # one stream: library kernels, NCCL ordering and the timing events
     torch.cuda.set_stream(stream)
     _lib.call("sk_set_stream", dev, stream.cuda_stream)
 
-    n, dtype = args.qubits, args.dtype
-    prog = compile_circuit(build_qft(n), dtype=dtype, device=dev)
-    nsw = prog.n_sweeps
+    n_local, dtype = args.qubits, args.dtype
+    sq = ShardedQFT(n_local, dtype)  # world == 1: the plain single-GPU QFT-n program
+    n, G = sq.n, sq.G
     elem = 8 if dtype == "c64" else 16
-    state_bytes = (1 << n) * elem
-
-    # random normalised input generated on the device (not timed)
-    g = torch.Generator(device=f"cuda:{dev}").manual_seed(1234 + rank)
-    st = DenseKet(n, dtype=dtype, device=dev)
+    slab_bytes = (1 << n_local) * elem
     real = torch.float32 if dtype == "c64" else torch.float64
-    x = torch.randn(2 << n, device=f"cuda:{dev}", dtype=real, generator=g)
-    x /= torch.linalg.vector_norm(x)
-    _lib.call("sk_copy_from_device", st._h, x.data_ptr(), 1 << n)  # torch is plumbing only
+
+    # random normalised global state, generated on the device per rank (not timed)
+    g = torch.Generator(device=f"cuda:{dev}").manual_seed(1234 + rank)
+    sq.state.copy_(torch.randn(2 << n_local, device=f"cuda:{dev}", dtype=real, generator=g))
+    sq.state.div_(torch.linalg.vector_norm(sq.state) * math.sqrt(world))
     torch.cuda.synchronize()
+
+    body, top = sq.body, sq.top
+    nb = body.n_sweeps
+
+    def step(evs=None):
+        if G:
+            sq._exchange()
+            _lib.call("sk_rebind", sq._h, sq.state.data_ptr())
+            _lib.call("sk_program_run", sq._h, top._h, 0, -1)
+            sq._exchange()
+        _lib.call("sk_rebind", sq._h, sq.state.data_ptr())
+        if evs is None:
+            _lib.call("sk_program_run", sq._h, body._h, 0, -1)
+        else:
+            evs[0].record(stream)
+            for i in range(nb):
+                _lib.call("sk_program_run", sq._h, body._h, i, 1)
+                evs[i + 1].record(stream)
 
     def barrier():
         if dist is not None:
@@ -189,58 +203,56 @@ def run_ours(args, rank: int, world: int):
         torch.cuda.synchronize()
 
     for _ in range(args.warmup):
-        prog.run(st)
+        step()
     barrier()
 
-    # timed region: K QFTs, events between sweeps for per-launch durations
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nsw + 1)] for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nb + 1)] for _ in range(args.steps)]
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev) as clk:
         barrier()
         start.record(stream)
         for k in range(args.steps):
-            evs[k][0].record(stream)
-            for s_ in range(nsw):
-                prog.run(st, s_, 1)
-                evs[k][s_ + 1].record(stream)
+            step(evs[k])
         stop.record(stream)
         torch.cuda.synchronize()
-        # keep the sampler alive a little so short regions still get samples
-        if len(clk.samples) < 20:
+        if len(clk.samples) < 20:  # keep sampling a little so short regions still get clock readings
             t_end = time.time() + 0.2
             while time.time() < t_end:
-                prog.run(st)
+                step()
             torch.cuda.synchronize()
     ms = start.elapsed_time(stop)
-    launch_ms = [evs[k][i].elapsed_time(evs[k][i + 1]) for k in range(args.steps) for i in range(nsw)]
+    launch_ms = [evs[k][i].elapsed_time(evs[k][i + 1]) for k in range(args.steps) for i in range(nb)]
     if dist is not None:
         t = torch.tensor([ms], device=f"cuda:{dev}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_per_step = ms / args.steps
-    value = world * qft_layers(n) / (ms_per_step / 1e3)
+    amp_layers = n * float(1 << n)  # n QFT layers over 2^n amplitudes, whole job
+    value = amp_layers / (ms_per_step / 1e3)
     avg_launch = statistics.mean(launch_ms)
-    per_launch_bytes = prog.bytes_per_sweep()
+    per_launch_bytes = body.bytes_per_sweep()
     achieved_gbs = per_launch_bytes / (avg_launch / 1e3) / 1e9
 
     # ---- e2e through the public API with host buffers --------------------
-    host = torch.empty(2 << n, dtype=real, pin_memory=True)
-    host.copy_(x)
-    del x
+    host = torch.empty(2 << n_local, dtype=real, pin_memory=True)
+    host.copy_(sq.state)
     out_host = torch.empty_like(host)
+
+    def e2e_step():
+        _lib.call("sk_rebind", sq._h, sq.state.data_ptr())
+        _lib.call("sk_upload_native", sq._h, host.data_ptr(), 1 << n_local)
+        step()
+        _lib.call("sk_rebind", sq._h, sq.state.data_ptr())
+        _lib.call("sk_download_native", sq._h, out_host.data_ptr(), 1 << n_local)
+
     for _ in range(2):
-        _lib.call("sk_upload_native", st._h, host.data_ptr(), 1 << n)
-        prog.run(st)
-        _lib.call("sk_download_native", st._h, out_host.data_ptr(), 1 << n)
+        e2e_step()
     e2e_steps = max(3, min(args.steps, 10))
     barrier()
-    t0 = time.perf_counter()
     e_start, e_stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e_start.record(stream)
     for _ in range(e2e_steps):
-        _lib.call("sk_upload_native", st._h, host.data_ptr(), 1 << n)
-        prog.run(st)
-        _lib.call("sk_download_native", st._h, out_host.data_ptr(), 1 << n)
+        e2e_step()
     e_stop.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e_start.elapsed_time(e_stop) / e2e_steps
@@ -260,29 +272,36 @@ def run_ours(args, rank: int, world: int):
             traffic = None
 
     if rank == 0:
-        cpu = cpu_baseline(n) if (world == 1 and not args.no_cpu) else None
+        cpu = cpu_baseline(n_local) if (world == 1 and not args.no_cpu) else None
         line = {
-            "metric": f"QFT-{n} gate-layers/s", "value": value, "unit": "gate-layers/s", "n_gpus": world,
+            "metric": "QFT amplitude-layer updates/s", "value": value, "unit": "amp-layers/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": dtype, "data": "synthetic",
-            "config": {"workload": f"exact QFT on {n} qubits, 1xB200 per rank (BASELINE configs[1])",
-                       "qubits": n, "state_bytes": state_bytes, "input": "random normalised state, device-generated",
-                       "l2": "state (1 GiB) > L2 (126 MB): no flush needed", "swaps": "label permutations",
-                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+            "config": {"workload": f"exact QFT on {n} qubits ({n_local} per GPU x {world} GPU"
+                                   f"{'s, global-qubit sharded' if world > 1 else ''}); BASELINE configs[1] at N=1",
+                       "qubits": n, "qubits_per_gpu": n_local, "state_bytes_per_gpu": slab_bytes,
+                       "input": "random normalised state, device-generated",
+                       "l2": "state (1 GiB per GPU) > L2 (126 MB): no flush needed",
+                       "swaps": "label permutations (engine.py:525-535)",
+                       "parallelism": f"global-qubit sharding over {world} GPUs (2 NCCL all-to-alls per QFT)"
+                                      if world > 1 else "single GPU"},
             "qft_sec": ms_per_step / 1e3,
-            "hbm_gbs": nsw * per_launch_bytes / (ms_per_step / 1e3) / 1e9,
-            "sweeps_per_qft": nsw,
-            "unfused_bytes_per_qft": 2 * elem * (n * (1 << n) + (n * (n - 1) // 2) * (1 << (n - 1))),
-            "gpu_launches": args.steps * nsw,
+            "qft_qubits": n,
+            "gate_layers_per_s": n / (ms_per_step / 1e3),
+            "hbm_gbs": nb * per_launch_bytes / (ms_per_step / 1e3) / 1e9,
+            "sweeps_per_qft": sq.launches(),
+            "exchange_bytes_per_gpu": sq.exchange_bytes(),
+            "unfused_bytes_per_qft_per_gpu": 2 * elem * (n * (1 << n_local) + (n * (n - 1) // 2) * (1 << (n_local - 1))),
+            "gpu_launches": args.steps * sq.launches(),
             "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": peak, "unit": "GB/s",
                          "frac": achieved_gbs / peak, "traffic": traffic,
-                         "kernel": "k_sweep<float,4>" if dtype == "c64" else "k_sweep<double,3>",
+                         "kernel": "k_sweep<float,4,qft>" if dtype == "c64" else "k_sweep<double,3,qft>",
                          "algorithmic_bytes_per_launch": per_launch_bytes, "avg_launch_ms": avg_launch,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
             "clocks": clk.summary(),
-            "e2e": {"value": world * qft_layers(n) / (e2e_ms / 1e3), "unit": "gate-layers/s",
-                    "h2d_bytes_per_step": state_bytes, "d2h_bytes_per_step": state_bytes,
-                    "ms_per_step": e2e_ms, "path": "sk_upload_native + sk_program_run + sk_download_native"},
+            "e2e": {"value": amp_layers / (e2e_ms / 1e3), "unit": "amp-layers/s",
+                    "h2d_bytes_per_step": slab_bytes * world, "d2h_bytes_per_step": slab_bytes * world,
+                    "ms_per_step": e2e_ms, "path": "sk_upload_native + QFT program(s) + sk_download_native"},
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)

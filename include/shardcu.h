@@ -66,6 +66,12 @@ int sk_create(int width, int dtype, int device, sk_state** out);
 int sk_create_from(int width, int dtype, int device, const double* host_c128, sk_state** out);
 int sk_copy(const sk_state* src, sk_state** out);
 int sk_destroy(sk_state* s);
+/* Non-owning view over caller device memory of 2^width native elements
+ * (torch / NCCL buffers for the sharded path); sk_destroy frees only the
+ * handle.  sk_rebind points a view at another buffer (e.g. after an
+ * out-of-place all-to-all). */
+int sk_wrap(int width, int dtype, int device, uint64_t ptr, sk_state** out);
+int sk_rebind(sk_state* s, uint64_t ptr);
 int sk_width(const sk_state* s, int* width);
 int sk_dtype(const sk_state* s, int* dtype);
 /* Raw device pointer of the amplitude array (for torch / NCCL plumbing). */

@@ -50,6 +50,8 @@ _SIGS = {
     "sk_create_from": [C.c_int, C.c_int, C.c_int, dptr, C.POINTER(p_state)],
     "sk_copy": [p_state, C.POINTER(p_state)],
     "sk_destroy": [p_state],
+    "sk_wrap": [C.c_int, C.c_int, C.c_int, C.c_uint64, C.POINTER(p_state)],
+    "sk_rebind": [p_state, C.c_uint64],
     "sk_width": [p_state, C.POINTER(C.c_int)],
     "sk_dtype": [p_state, C.POINTER(C.c_int)],
     "sk_device_ptr": [p_state, C.POINTER(C.c_uint64)],

@@ -69,6 +69,7 @@ struct sk_state {
   int device = 0;
   int64_t n = 0;  // 2^width amplitudes
   size_t elem = 16;
+  bool owned = true;  // false for sk_wrap views over caller memory
 };
 
 namespace sk {

@@ -663,8 +663,34 @@ int sk_destroy(sk_state* s) {
   if (!s) return SK_OK;
   DevCtx* c;
   SK_TRY(ctx_get(s->device, &c));
-  if (s->d) SK_CUDA(cudaFreeAsync(s->d, c->stream));
+  if (s->d && s->owned) SK_CUDA(cudaFreeAsync(s->d, c->stream));
   delete s;
+  return SK_OK;
+}
+
+int sk_wrap(int width, int dtype, int device, uint64_t ptr, sk_state** out) {
+  if (width < 1 || width > 40) return set_error(SK_EVALUE, "bad width %d", width);
+  if (dtype != SK_C64 && dtype != SK_C128) return set_error(SK_EVALUE, "bad dtype %d", dtype);
+  if (!ptr || (ptr & 15)) return set_error(SK_EVALUE, "wrapped buffer must be non-null and 16-byte aligned");
+  DevCtx* c;
+  SK_TRY(ctx_get(device, &c));
+  sk_state* s = new sk_state();
+  s->d = (void*)ptr;
+  s->width = width;
+  s->dtype = dtype;
+  s->device = device;
+  s->n = (int64_t)1 << width;
+  s->elem = elem_size(dtype);
+  s->owned = false;
+  *out = s;
+  return SK_OK;
+}
+
+int sk_rebind(sk_state* s, uint64_t ptr) {
+  SK_TRY(check_state(s));
+  if (s->owned) return set_error(SK_EVALUE, "only sk_wrap views can be rebound");
+  if (!ptr || (ptr & 15)) return set_error(SK_EVALUE, "wrapped buffer must be non-null and 16-byte aligned");
+  s->d = (void*)ptr;
   return SK_OK;
 }
 

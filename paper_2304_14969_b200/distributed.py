@@ -1,0 +1,167 @@
+"""Global-qubit sharding of the QFT over 2^G ranks.
+
+An n-qubit state is split by its top G index bits ("global" qubits): rank r
+holds the 2^(n-G) amplitudes whose top bits equal r.  The reference has no
+distributed path; this is the B200-native extension that makes QFT-37 fit on
+8 GPUs.  The QFT needs exactly two exchanges:
+
+  A. all-to-all swapping the global bits [n-G, n) with the top local bits
+     [n-2G, n-G) (equal 2^(n-2G)-amplitude blocks: block b of rank r goes to
+     rank b, slot r) — the top G logical qubits become local;
+  1. one generic fused sweep applies QFT layers j = n-1 .. n-G.  Their CP fans
+     split into a local RAMP over bits [0, n-2G), a local RAMP over the moved
+     top qubits, and a phase that is a rank constant (the fan's contribution
+     from the now-global logical qubits [n-2G, n-G));
+  B. the same all-to-all again: the layout is the identity once more;
+  2. layers j < n-G have all their controls local: each rank runs exactly the
+     (n-G)-qubit QFT body (the FFT-form fused sweeps of fusion.plan_qft).
+
+The QFT's final SWAP layer stays a label permutation (full bit reversal).
+Exchanges go through torch.distributed (NCCL over NVLink on the box; gloo in
+the CPU tests), on torch buffers wrapped as non-owning sk_state views.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import numpy as np
+
+from . import _lib, fusion
+from .circuit import gate_matrix
+
+
+def layout(n_local: int, world: int) -> tuple[int, int]:
+    """(n, G) for `world` ranks of 2^n_local amplitudes each."""
+    G = world.bit_length() - 1
+    if world < 1 or (1 << G) != world:
+        raise ValueError(f"world size must be a power of two, got {world}")
+    if G and n_local < 2 * G + 1:
+        raise ValueError(f"need n_local >= 2G+1 ({2 * G + 1}) local qubits, got {n_local}")
+    return n_local + G, G
+
+
+def top_layer_ops(n_local: int, G: int, rank: int) -> list[fusion.Op]:
+    """Ops (local physical bits) of QFT layers j = n-1..n-G after exchange A."""
+    n = n_local + G
+    lo2 = n - 2 * G
+    ops: list[fusion.Op] = []
+    h = fusion._m8(gate_matrix("h"))
+    for j in range(n - 1, n - G - 1, -1):
+        P = j - G
+        ops.append(fusion.Op(fusion.MAT, P, h))
+        if lo2 >= 1:  # controls [0, n-2G): local, weights 2^(i-j)
+            ops.append(fusion.Op(fusion.RAMP, 0, (2.0 ** -j, 0, 0, 0, 0, 0, 0, 0), 1 << P, 1 << P, nbits=lo2))
+        # controls [n-2G, n-G) now sit in the rank bits: a rank-constant phase on P
+        theta = sum(math.pi * 2.0 ** (i - j) for i in range(lo2, n - G) if (rank >> (i - lo2)) & 1)
+        if theta:
+            ops.append(fusion.Op(fusion.DIAG, P, (1.0, 0, 0, 0, 0, 0, math.cos(theta), math.sin(theta))))
+        if P - lo2 >= 1:  # controls [n-G, j) moved to local [n-2G, P): weights 2^(p-P)
+            ops.append(fusion.Op(fusion.RAMP, lo2, (2.0 ** (lo2 - P), 0, 0, 0, 0, 0, 0, 0), 1 << P, 1 << P,
+                                 nbits=P - lo2))
+    return ops
+
+
+def plans(n_local: int, world: int, rank: int, dtype: str = "c64"):
+    """(top-layer plan or None, local QFT-body plan) for one rank."""
+    n, G = layout(n_local, world)
+    body = fusion.plan_qft(n_local, dtype)
+    if G == 0:
+        return None, body
+    top = fusion.plan_ops(top_layer_ops(n_local, G, rank), n_local, dtype)
+    return top, body
+
+
+def final_order(n: int) -> list[int]:
+    """permute_qubits order mapping the physical result to label order (the
+    QFT's reversal swaps as a label permutation)."""
+    return list(reversed(range(n)))
+
+
+def exchange_blocks(slabs: list[np.ndarray]) -> list[np.ndarray]:
+    """all_to_all_single semantics on equal blocks, for the NumPy emulation:
+    out[r] block s = in[s] block r."""
+    W = len(slabs)
+    blocks = [np.split(s, W) for s in slabs]
+    return [np.concatenate([blocks[s][r] for s in range(W)]) for r in range(W)]
+
+
+def emulate(slabs: list[np.ndarray], dtype: str = "c64") -> list[np.ndarray]:
+    """Single-process NumPy emulation of the sharded QFT (all ranks), used by
+    the CPU tests to check the plan/exchange logic against the oracle."""
+    W = len(slabs)
+    n_local = int(slabs[0].size).bit_length() - 1
+    n, G = layout(n_local, W)
+    cur = [s.copy() for s in slabs]
+    if G:
+        cur = exchange_blocks(cur)
+        for r in range(W):
+            top, _ = plans(n_local, W, r, dtype)
+            fusion.run_plan_numpy(top, cur[r])
+        cur = exchange_blocks(cur)
+    for r in range(W):
+        _, body = plans(n_local, W, r, dtype)
+        fusion.run_plan_numpy(body, cur[r])
+    return cur
+
+
+class ShardedQFT:
+    """Device execution on one rank: two torch buffers (the state and the
+    exchange target) wrapped as sk_state views; NCCL all_to_all_single for
+    the exchanges; fused sweeps for the local work."""
+
+    def __init__(self, n_local: int, dtype: str = "c64", group=None):
+        import torch
+        import torch.distributed as dist
+
+        from .executor import Program
+        self.torch, self.dist, self.group = torch, dist, group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.n_local, self.dtype = n_local, dtype
+        self.n, self.G = layout(n_local, self.world)
+        self.device = torch.cuda.current_device()
+        real = torch.float32 if dtype == "c64" else torch.float64
+        self.bufs = [torch.empty(2 << n_local, dtype=real, device=f"cuda:{self.device}") for _ in range(2)]
+        self.cur = 0
+        h = C.c_void_p()
+        _lib.call("sk_wrap", n_local, _lib.DTYPES[dtype], self.device, self.bufs[0].data_ptr(), C.byref(h))
+        self._h = h
+        top, body = plans(n_local, self.world, self.rank, dtype)
+        self.top = Program(top, self.device) if top is not None else None
+        self.body = Program(body, self.device)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and _lib._lib is not None:
+            _lib._lib.sk_destroy(h)
+
+    @property
+    def state(self):
+        return self.bufs[self.cur]
+
+    def _exchange(self):
+        nxt = 1 - self.cur
+        self.dist.all_to_all_single(self.bufs[nxt], self.bufs[self.cur], group=self.group)
+        self.cur = nxt
+
+    def run(self, events=None):
+        """One sharded QFT body on this rank's slab (stream-ordered on the
+        current torch stream; libshardcu must be bound to it)."""
+        if self.G:
+            self._exchange()
+            _lib.call("sk_rebind", self._h, self.state.data_ptr())
+            _lib.call("sk_program_run", self._h, self.top._h, 0, -1)
+            self._exchange()
+        _lib.call("sk_rebind", self._h, self.state.data_ptr())
+        _lib.call("sk_program_run", self._h, self.body._h, 0, -1)
+
+    def launches(self) -> int:
+        return (self.top.n_sweeps if self.top else 0) + self.body.n_sweeps
+
+    def exchange_bytes(self) -> int:
+        """Bytes each rank sends per QFT (two all-to-alls, own block stays)."""
+        if not self.G:
+            return 0
+        elem = 8 if self.dtype == "c64" else 16
+        return 2 * (self.world - 1) * ((1 << self.n_local) // self.world) * elem
