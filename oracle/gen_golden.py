@@ -212,11 +212,85 @@ def gen_qft():
     np.savez_compressed(OUT / "qft_dense.npz", **d)
 
 
+def gen_engine():
+    """Reference HybridState runs (stabilizer path off and default flags) that
+    the device engine must reproduce decision for decision."""
+    d = {}
+    none = reng.OptFlags.none()
+    nostab = reng.OptFlags(stabilizer_hybrid=False)
+    cases = []
+    for i in range(6):
+        w, dep = [(6, 4), (8, 6), (10, 8), (12, 10), (9, 12), (14, 6)][i]
+        seed = rv.derive_seed(5, i)
+        for p in (0.0, 0.3, 0.6, 1.0):
+            for fl_name, fl in (("nostab", nostab), ("default", reng.OptFlags()), ("none", none)):
+                if fl_name == "none" and p not in (0.0, 0.6):
+                    continue
+                cases.append((f"rc{i}_p{int(p * 10)}_{fl_name}", w, dep, seed, p, 1 << 12, fl))
+    for name, w, dep, seed, p, budget, fl in cases:
+        c = rc.build_random_circuit(w, dep, seed)
+        cfg = reng.EngineConfig(sdrp=p, mem_budget=budget, rng_seed=seed, optimizations=fl)
+        key = f"eng/{name}"
+        d[f"{key}/spec"] = np.array([w, dep, seed, budget], dtype=np.uint64)
+        d[f"{key}/p"] = p
+        d[f"{key}/flags"] = np.array([fl.control_elimination, fl.hx_commutation, fl.label_swap,
+                                      fl.pauli_coalescing, fl.stabilizer_hybrid], dtype=bool)
+        try:
+            sim = rv.run_hybrid(c, cfg)
+            sim.flush_all()
+            d[f"{key}/ok"] = True
+            d[f"{key}/eps"] = np.array(sim.eps_record, dtype=float)
+            d[f"{key}/fmodel"] = sim.estimated_fidelity()
+            d[f"{key}/peak"] = sim.peak_amplitudes
+            d[f"{key}/stats"] = np.array([sim.stats[k] for k in ("label_swaps", "kernels", "eliminated_controls",
+                                                                 "merges", "splits")])
+            d[f"{key}/ket"] = sim.full_ket().amps
+        except reng.MemoryBudgetError as exc:
+            d[f"{key}/ok"] = False
+            d[f"{key}/needed"] = exc.needed
+    # QFT on GHZ through the engine (the paper's Fig. 1b path), n = 8
+    for n in (6, 9):
+        sim = reng.HybridState(n, reng.EngineConfig(mem_budget=1 << 20, optimizations=nostab))
+        sim.apply_circuit(rc.build_ghz(n))
+        sim.apply_circuit(rc.build_qft(n))
+        d[f"engqft/{n}/ket"] = sim.full_ket().amps
+        d[f"engqft/{n}/stats"] = np.array([sim.stats[k] for k in ("label_swaps", "kernels", "eliminated_controls",
+                                                                  "merges", "splits")])
+    # measurement, collapse and sampling with the engine rng
+    for i in range(3):
+        w = 7 + i
+        seed = 100 + i
+        c = rc.build_random_circuit(w, 5, seed)
+        gates = list(c.gates)
+        gates.insert(len(gates) // 2, rc.measure(2))
+        cm = rc.Circuit(w, tuple(gates))
+        sim = reng.HybridState(w, reng.EngineConfig(rng_seed=seed, optimizations=nostab))
+        sim.apply_circuit(cm)
+        d[f"meas/{i}/spec"] = np.array([w, seed], dtype=np.uint64)
+        d[f"meas/{i}/samples"] = np.array([int(b[::-1], 2) for b in sim.sample(300)], dtype=np.int64)
+        d[f"meas/{i}/measure_all"] = np.array([int(sim.measure_all()[::-1], 2)])
+    # min-SDRP searches (validate.py:280-300), incl. 54 qubits x 7 layers
+    for (w, dep, i, budget) in ((16, 6, 0, 1 << 10), (16, 8, 1, 1 << 10), (54, 7, 2, 1 << 18)):
+        seed = rv.derive_seed(0, i)
+        r = rv.min_sdrp_search(w, dep, seed, budget)
+        d[f"minsdrp/{w}_{dep}_{i}/spec"] = np.array([w, dep, seed, budget], dtype=np.uint64)
+        d[f"minsdrp/{w}_{dep}_{i}/res"] = np.array([r.feasible, -1 if r.p_min is None else r.p_min,
+                                                    -1 if r.f_model is None else r.f_model, r.peak_amplitudes],
+                                                   dtype=float)
+        if r.feasible:
+            sim = rv.run_hybrid(rc.build_random_circuit(w, dep, seed),
+                                reng.EngineConfig(sdrp=r.p_min, mem_budget=budget, rng_seed=seed))
+            sim.flush_all()
+            d[f"minsdrp/{w}_{dep}_{i}/eps"] = np.array(sim.eps_record)
+    np.savez_compressed(OUT / "engine.npz", **d)
+
+
 if __name__ == "__main__":
     OUT.mkdir(parents=True, exist_ok=True)
     assert shardsim.RNG_ALGORITHM == "pcg64"
     gen_circuits()
     gen_ket()
     gen_qft()
+    gen_engine()
     for p in sorted(OUT.glob("*.npz")):
         print(p.name, p.stat().st_size)

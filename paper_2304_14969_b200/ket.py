@@ -253,6 +253,21 @@ class DenseKet:
         amplitude_writes += 1 << (self.width - 1)
         return bloch_from_sums(out[0:4]), bloch_from_sums(out[4:8])
 
+    def apply_controlled_bloch_sums(self, control: int, polarity: int, target: int, m):
+        """As `apply_controlled_bloch` but returning the raw sums
+        (Re, Im of sum conj(a0) a1, sum |a0|^2, sum |a1|^2) of control and target."""
+        global amplitude_writes
+        if control == target:
+            raise ValueError(f"overlapping qubit indices {(control, target)}")
+        m = _as_mat(m)
+        _check_unitary(m)
+        self._axis(control)
+        self._axis(target)
+        out = (C.c_double * 8)()
+        call("sk_apply_controlled_bloch", self._h, control, int(polarity), target, _lib.mat8(m), out)
+        amplitude_writes += 1 << (self.width - 1)
+        return tuple(out[0:4]), tuple(out[4:8])
+
     def apply_pauli_layer(self, ops) -> None:
         """Simultaneous Paulis [(qubit, 'x'|'y'|'z'), ...] in one pass (ket.py:166-202)."""
         global amplitude_writes

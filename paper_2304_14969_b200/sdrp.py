@@ -1,0 +1,79 @@
+"""SDRP drivers over the device engine (the reference's validate.py:114-300
+callers of the hot path): run a circuit through the hybrid engine, the exact
+overlap fidelity against the fused dense executor, and the minimum-SDRP
+search that config 5 (54 qubits, 7-10 layers) is quoted on."""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+
+from .circuit import Circuit, build_random_circuit
+from .engine import EngineConfig, HybridState
+from .errors import MemoryBudgetError
+from .executor import dense_reference
+from .ket import DenseKet
+
+DEFAULT_P_STEP = 0.025
+
+
+def run_hybrid(c: Circuit, cfg: EngineConfig, initial: DenseKet | None = None) -> HybridState:
+    """validate.py:114-121."""
+    sim = HybridState(c.width, cfg)
+    if initial is not None:
+        sim.load_state(initial)
+    sim.apply_circuit(c)
+    return sim
+
+
+def exact_fidelity(c: Circuit, cfg: EngineConfig) -> tuple[float, float]:
+    """(exact overlap with the plain dense simulation, engine estimate); validate.py:124-128."""
+    exact = dense_reference(c, dtype=cfg.dtype)
+    sim = run_hybrid(c, cfg)
+    return sim.full_ket().fidelity(exact), sim.estimated_fidelity()
+
+
+@dataclass(frozen=True)
+class MinSdrpResult:
+    feasible: bool
+    p_min: float | None
+    f_model: float | None
+    peak_amplitudes: int = 0
+
+
+@dataclass
+class SdrpRun:
+    p: float
+    ok: bool
+    f_model: float | None
+    peak_amplitudes: int
+    rounds: int
+    wall_s: float
+
+
+def min_sdrp_search(width: int, depth: int, seed: int, mem_budget: int, p_step: float = DEFAULT_P_STEP,
+                    dtype: str = "c128", trace: list | None = None) -> MinSdrpResult:
+    """Lower p from 1 in p_step decrements until the budget fails; report the
+    last completing run (validate.py:280-300)."""
+    if p_step <= 0:
+        raise ValueError("p_step must be > 0")
+    c = build_random_circuit(width, depth, seed)
+    best = None
+    steps = int(round(1.0 / p_step))
+    for i in range(steps, -1, -1):
+        p = round(i * p_step, 9)
+        cfg = EngineConfig(sdrp=p, mem_budget=mem_budget, rng_seed=seed, dtype=dtype)
+        t0 = time.perf_counter()
+        try:
+            sim = run_hybrid(c, cfg)
+            sim.flush_all()
+        except MemoryBudgetError as exc:
+            if trace is not None:
+                trace.append(SdrpRun(p, False, None, exc.needed, 0, time.perf_counter() - t0))
+            return best if best is not None else MinSdrpResult(False, None, None)
+        if trace is not None:
+            trace.append(SdrpRun(p, True, sim.estimated_fidelity(), sim.peak_amplitudes, len(sim.eps_record),
+                                 time.perf_counter() - t0))
+        best = MinSdrpResult(True, p, sim.estimated_fidelity(), sim.peak_amplitudes)
+        if p == 0.0:
+            break
+    return best

@@ -126,3 +126,20 @@ def test_random_circuits_dense(golden):
         x[0] = 1
         out = O.dense_run(build_random_circuit(w, d, s).gates, x, gate_matrix)
         assert np.array_equal(out, g[key.replace("/spec", "/out")])
+
+
+def test_reference_engine_stabilizer_path_is_decision_neutral_on_random_circuits(golden):
+    """Recorded fact backing the dense-only engine: on the random-circuit
+    workloads the reference engine makes the same SDRP decisions (eps record,
+    peak, OOM point) with and without its stabilizer path."""
+    g = golden("engine")
+    keys = sorted({k.rsplit("/", 1)[0] for k in g.files if k.startswith("eng/") and k.endswith("_nostab")})
+    assert len(keys) >= 20
+    for k in keys:
+        k2 = k.replace("_nostab", "_default")
+        assert bool(g[k + "/ok"]) == bool(g[k2 + "/ok"])
+        if bool(g[k + "/ok"]):
+            assert np.array_equal(g[k + "/eps"], g[k2 + "/eps"])
+            assert int(g[k + "/peak"]) == int(g[k2 + "/peak"])
+        else:
+            assert int(g[k + "/needed"]) == int(g[k2 + "/needed"])
