@@ -27,6 +27,7 @@
 // tau = exp(2 pi i frac(F * turn / 2^64)), F a bit field of the thread's
 // index, `turn` the RAMP scale in 64-bit fixed-point turns: exact modular
 // arithmetic, then one MUFU sin/cos (fp32) or sincospi (fp64) per thread.
+#include <cstdlib>
 #include <vector>
 
 #include "sk_internal.cuh"
@@ -528,6 +529,214 @@ __global__ void __launch_bounds__(512, 2) k_sweep(vec2_t<R>* __restrict__ amps, 
   }
 }
 
+// ---------------------------------------------------------------------------
+// k_qft: the QFT-window sweep with every chunk parameter in the (constant-
+// bank) kernel argument instead of an op stream, and packed arithmetic
+// (PK<R>: FADD2/FMUL2/FFMA2 for fp32).  Same math as qft_chunk above — the
+// host builds its QSweep from the same lowered K_QFTS ops
+// (qsweep_from), so tests/test_kernel_lowering.py's emulation covers both.
+// Per amplitude and 4-layer chunk: 4 paired adds for the butterflies, ~1.25
+// paired multiply pairs for the compile-time internal twiddles, and 4 paired
+// ops per Gray-walked entry / end phase.
+// ---------------------------------------------------------------------------
+constexpr int kQRuns = 4;
+
+struct QStage {
+  int code;  // L * 8 + TOP of the stage's chunk; 0 = no chunk (store stage)
+  uint32_t flags;
+  int lo, ng, nl, pad;
+  uint64_t tmask, tval, qmask;
+  double scale;
+  Run grun[kQRuns], lrun[kQRuns];
+  uint64_t reg_goff[kMaxR];
+  uint32_t reg_soff[kMaxR];
+};
+
+struct QSweep {
+  int ntile, nstages, nb, pad;
+  Run brun[kQRuns];
+  QStage st[kMaxS];
+};
+
+__device__ __forceinline__ uint64_t deposit_q(uint64_t x, const Run* r, int n) {
+  uint64_t o = 0;
+#pragma unroll
+  for (int i = 0; i < kQRuns; ++i)
+    if (i < n) o |= ((x >> r[i].src) & ((1ull << r[i].w) - 1)) << r[i].dst;
+  return o;
+}
+
+__device__ __forceinline__ uint32_t deposit_q32(uint32_t x, const Run* r, int n) {
+  uint32_t o = 0;
+#pragma unroll
+  for (int i = 0; i < kQRuns; ++i)
+    if (i < n) o |= ((x >> r[i].src) & ((1u << r[i].w) - 1)) << r[i].dst;
+  return o;
+}
+
+template <typename R, int K>
+__device__ __forceinline__ vec2_t<R> pk_pi8(vec2_t<R> x) {  // x * exp(i pi K / 8), K compile-time
+  if constexpr (K == 0) return x;
+  else if constexpr (K == 4) return mk<R>(-x.y, x.x);
+  else {
+    constexpr double c = K == 1 ? 0.92387953251128674 : K == 2 ? 0.70710678118654752 : K == 3 ? 0.38268343236508978
+                       : K == 5 ? -0.38268343236508978 : K == 6 ? -0.70710678118654752 : -0.92387953251128674;
+    constexpr double s = K == 1 ? 0.38268343236508978 : K == 2 ? 0.70710678118654752 : K == 3 ? 0.92387953251128674
+                       : K == 5 ? 0.92387953251128674 : K == 6 ? 0.70710678118654752 : 0.38268343236508978;
+    return PK<R>::mul(x, mk<R>((R)c, (R)s));
+  }
+}
+
+template <typename R, int NR, int L, int TOP, int P, int E>
+__device__ __forceinline__ void pk_pair(vec2_t<R> (&a)[1 << NR]) {
+  if constexpr (E < (1 << NR)) {
+    if constexpr (!((E >> P) & 1)) {
+      constexpr int E1 = E | (1 << P);
+      const vec2_t<R> s = PK<R>::add(a[E], a[E1]);
+      const vec2_t<R> d = PK<R>::sub(a[E], a[E1]);
+      a[E] = s;
+      a[E1] = pk_pi8<R, qft_k8<NR, L, TOP, P, E>()>(d);
+    }
+    pk_pair<R, NR, L, TOP, P, E + 1>(a);
+  }
+}
+
+template <typename R, int NR, int L, int TOP, int P>
+__device__ __forceinline__ void pk_layers(vec2_t<R> (&a)[1 << NR]) {
+  if constexpr (P >= TOP - L + 1 && P >= 0) {
+    pk_pair<R, NR, L, TOP, P, 0>(a);
+    pk_layers<R, NR, L, TOP, P - 1>(a);
+  }
+}
+
+// a[e] *= phase(base + sum_{chunk slots p} e_p u_p) * scale, Gray-walked:
+// per element one paired multiply to step the phase and one to apply it
+template <typename R, int NR, int L, int TOP>
+__device__ __forceinline__ void pk_phase(vec2_t<R> (&a)[1 << NR], uint64_t base, const uint64_t (&ut)[NR], R scale) {
+  using P = PK<R>;
+  vec2_t<R> u[NR], uc[NR];
+#pragma unroll
+  for (int p = 0; p < NR; ++p)
+    if (p >= TOP - L + 1 && p <= TOP) {
+      u[p] = turn_phase<R>(ut[p]);
+      uc[p] = P::conj(u[p]);
+    }
+  vec2_t<R> w = P::scale(turn_phase<R>(base), scale);
+  a[0] = P::mul(a[0], w);
+#pragma unroll
+  for (int k = 1; k < (1 << NR); ++k) {
+    const int b = ctz_c(k);
+    const int e = k ^ (k >> 1);
+    if (b >= TOP - L + 1 && b <= TOP) w = P::mul(w, ((e >> b) & 1) ? u[b] : uc[b]);
+    a[e] = P::mul(a[e], w);
+  }
+}
+
+template <typename R, int NR, int L, int TOP>
+__device__ __forceinline__ void pk_chunk(const QStage& st, vec2_t<R> (&a)[1 << NR], uint64_t gthr) {
+  if constexpr (L >= 1 && L <= NR && TOP < NR && TOP - L + 1 >= 0) {
+    constexpr int B0 = TOP - L + 1;
+    const unsigned fl = st.flags;
+    const R scale = (R)st.scale;
+    bool scaled = !(fl & F_SCALE);
+    const uint64_t lv = gthr & st.qmask;
+    if (fl & F_ENTRY) {
+      const uint64_t th_all = __brevll(gthr & st.tmask), th_new = __brevll(gthr & st.tval);
+      uint64_t ut[NR];
+#pragma unroll
+      for (int p = 0; p < NR; ++p) ut[p] = (p >= B0 && p <= TOP) ? th_all << ((st.lo + p - B0) & 63) : 0;
+      const bool here = !scaled && !(fl & F_END);
+      pk_phase<R, NR, L, TOP>(a, th_new * lv, ut, here ? scale : (R)1);
+      scaled = scaled || here;
+    }
+    pk_layers<R, NR, L, TOP, TOP>(a);
+    if (fl & F_END) {
+      uint64_t ut[NR];
+#pragma unroll
+      for (int p = 0; p < NR; ++p) ut[p] = (p >= B0 && p <= TOP) ? lv << ((63 - (st.lo + p - B0)) & 63) : 0;
+      pk_phase<R, NR, L, TOP>(a, 0, ut, scaled ? (R)1 : scale);
+      scaled = true;
+    }
+    if (!scaled) {
+#pragma unroll
+      for (int e = 0; e < (1 << NR); ++e) a[e] = PK<R>::scale(a[e], scale);
+    }
+  }
+}
+
+// fp64 gets the larger register budget (its tiles are 2^(T-3) <= 256 threads)
+template <typename R>
+constexpr int qft_max_threads() { return sizeof(R) == 4 ? 512 : 256; }
+
+template <typename R, int NR>
+__global__ void __launch_bounds__(qft_max_threads<R>(), 2) k_qft(vec2_t<R>* __restrict__ amps, const __grid_constant__ QSweep sw) {
+  using V = vec2_t<R>;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  constexpr int NE = 1 << NR;
+  constexpr int SB = sizeof(V) == 8 ? 4 : 3;
+  const uint32_t tid = threadIdx.x;
+  const uint64_t base = deposit_q(blockIdx.x, sw.brun, sw.nb);
+
+  V a[NE];
+  const int ns = sw.nstages;
+  for (int s = 0; s < ns; ++s) {
+    const QStage& st = sw.st[s];
+    const uint64_t gthr = base | deposit_q(tid, st.grun, st.ng);
+    if (s == 0) {
+      const char* p = reinterpret_cast<const char*>(amps + gthr);
+#pragma unroll
+      for (int k = 0; k < NE; ++k) {
+        const int e = k ^ (k >> 1);
+        if (k) {
+          const int b = ctz_c(k);
+          p = ((e >> b) & 1) ? p + st.reg_goff[b] : p - st.reg_goff[b];
+        }
+        a[e] = *reinterpret_cast<const V*>(p);
+      }
+    } else {
+      __syncthreads();
+      uint32_t so = swz<SB>(deposit_q32(tid, st.lrun, st.nl)) * (uint32_t)sizeof(V);
+#pragma unroll
+      for (int k = 0; k < NE; ++k) {
+        const int e = k ^ (k >> 1);
+        if (k) so ^= st.reg_soff[ctz_c(k)];
+        a[e] = *reinterpret_cast<const V*>(smraw + so);
+      }
+    }
+    switch (st.code) {
+#define SK_QC(L, TOP) \
+  case L * 8 + TOP: pk_chunk<R, NR, L, TOP>(st, a, gthr); break;
+      SK_QC(1, 0) SK_QC(1, 1) SK_QC(1, 2) SK_QC(1, 3)
+      SK_QC(2, 1) SK_QC(2, 2) SK_QC(2, 3)
+      SK_QC(3, 2) SK_QC(3, 3)
+      SK_QC(4, 3)
+#undef SK_QC
+      default: break;
+    }
+    if (s == ns - 1) {
+      char* p = reinterpret_cast<char*>(amps + gthr);
+#pragma unroll
+      for (int k = 0; k < NE; ++k) {
+        const int e = k ^ (k >> 1);
+        if (k) {
+          const int b = ctz_c(k);
+          p = ((e >> b) & 1) ? p + st.reg_goff[b] : p - st.reg_goff[b];
+        }
+        *reinterpret_cast<V*>(p) = a[e];
+      }
+    } else {
+      if (s > 0) __syncthreads();
+      uint32_t so = swz<SB>(deposit_q32(tid, st.lrun, st.nl)) * (uint32_t)sizeof(V);
+#pragma unroll
+      for (int k = 0; k < NE; ++k) {
+        const int e = k ^ (k >> 1);
+        if (k) so ^= st.reg_soff[ctz_c(k)];
+        *reinterpret_cast<V*>(smraw + so) = a[e];
+      }
+    }
+  }
+}
+
 // register bits per stage: 16 fp32 amplitudes (32 regs) or 8 fp64 (32 regs)
 constexpr int kNR32 = 4;
 constexpr int kNR64 = 3;
@@ -830,6 +1039,43 @@ static void pack_kops(std::vector<HostKOp>& h, std::vector<unsigned char>& buf, 
   }
 }
 
+// QSweep for k_qft from a lowered QFT-only sweep: at most one K_QFTS op per
+// stage and at most kQRuns bit runs per mapping; false = keep k_sweep
+static bool qsweep_from(const DSweep& d, const std::vector<HostKOp>& kops, QSweep* q) {
+  *q = QSweep{};
+  if (!d.qft_only || d.nb > kQRuns) return false;
+  q->ntile = d.ntile;
+  q->nstages = d.nstages;
+  q->nb = d.nb;
+  for (int i = 0; i < d.nb; ++i) q->brun[i] = d.brun[i];
+  for (int s = 0; s < d.nstages; ++s) {
+    const DStage& a = d.st[s];
+    QStage& b = q->st[s];
+    if (a.ng > kQRuns || a.nl > kQRuns || a.op_end - a.op_begin > 1) return false;
+    b.ng = a.ng;
+    b.nl = a.nl;
+    for (int i = 0; i < a.ng; ++i) b.grun[i] = a.grun[i];
+    for (int i = 0; i < a.nl; ++i) b.lrun[i] = a.lrun[i];
+    for (int p = 0; p < kMaxR; ++p) {
+      b.reg_goff[p] = a.reg_goff[p];
+      b.reg_soff[p] = a.reg_soff[p];
+    }
+    b.code = 0;
+    if (a.op_end > a.op_begin) {
+      const HostKOp& k = kops[a.op_begin];
+      if (k.kind != K_QFTS) return false;
+      b.code = k.nbits * 8 + k.slot;
+      b.flags = k.flags;
+      b.lo = k.lo;
+      b.tmask = k.tmask;
+      b.tval = k.tval;
+      b.qmask = k.qmask;
+      b.scale = k.m[0];
+    }
+  }
+  return true;
+}
+
 }  // namespace sk
 
 struct sk_program {
@@ -838,11 +1084,22 @@ struct sk_program {
   int device = 0;
   int nr = 0;
   std::vector<sk::DSweep> sweeps;
+  std::vector<sk::QSweep> qsweeps;  // per sweep: k_qft arguments (valid when qft_ok[i])
+  std::vector<char> qft_ok;
   void* d_ops = nullptr;
   int nkops = 0;
 };
 
 using namespace sk;
+
+// SK_QFT_KERNEL=0 runs QFT windows through the generic k_sweep (A/B timing)
+static bool use_qft_kernel() {
+  static const int v = [] {
+    const char* e = std::getenv("SK_QFT_KERNEL");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v != 0;
+}
 
 template <typename R, int NR>
 static int launch_sweeps(sk_state* s, const sk_program* p, int first, int count, DevCtx* c) {
@@ -850,6 +1107,7 @@ static int launch_sweeps(sk_state* s, const sk_program* p, int first, int count,
   if (!attr_set[s->device]) {
     SK_CUDA(cudaFuncSetAttribute(k_sweep<R, NR, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     SK_CUDA(cudaFuncSetAttribute(k_sweep<R, NR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    SK_CUDA(cudaFuncSetAttribute(k_qft<R, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     attr_set[s->device] = true;
   }
   for (int i = first; i < first + count; ++i) {
@@ -859,7 +1117,9 @@ static int launch_sweeps(sk_state* s, const sk_program* p, int first, int count,
     const unsigned threads = 1u << (T - NR);
     const size_t smem = ((size_t)1 << T) * sizeof(vec2_t<R>);
     if (tiles > 0x7fffffffull) return set_error(SK_EVALUE, "too many tiles (%d bits outside the tile)", s->width - T);
-    if (d.qft_only)
+    if (p->qft_ok[i] && threads <= (unsigned)qft_max_threads<R>() && use_qft_kernel())
+      k_qft<R, NR><<<(unsigned)tiles, threads, smem, c->stream>>>((vec2_t<R>*)s->d, p->qsweeps[i]);
+    else if (d.qft_only)
       k_sweep<R, NR, true><<<(unsigned)tiles, threads, smem, c->stream>>>((vec2_t<R>*)s->d, d, (const KOp<R>*)p->d_ops);
     else
       k_sweep<R, NR, false><<<(unsigned)tiles, threads, smem, c->stream>>>((vec2_t<R>*)s->d, d, (const KOp<R>*)p->d_ops);
@@ -980,6 +1240,9 @@ int sk_program_create(int width, int dtype, int device, const sk_sweep* sweeps, 
   prog->dtype = dtype;
   prog->device = device;
   prog->nr = NR;
+  prog->qsweeps.resize(dsw.size());
+  prog->qft_ok.resize(dsw.size());
+  for (size_t i = 0; i < dsw.size(); ++i) prog->qft_ok[i] = qsweep_from(dsw[i], kops, &prog->qsweeps[i]);
   prog->sweeps = std::move(dsw);
   prog->nkops = (int)kops.size();
   if (!buf.empty()) {

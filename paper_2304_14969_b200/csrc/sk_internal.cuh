@@ -108,6 +108,40 @@ __device__ __forceinline__ vec2_t<R> cmad2(vec2_t<R> m0, vec2_t<R> a, vec2_t<R> 
   return mk<R>(x, y);
 }
 
+// Packed complex arithmetic.  For float2 every op is one or two sm_100
+// paired-fp32 instructions (FADD2 / FMUL2 / FFMA2; the swizzles and the
+// one-lane negation of the product term are free operand modifiers), so a
+// complex multiply is 2 issue slots instead of 4 and an add 1 instead of 2.
+// double2 falls back to scalar fp64.
+template <typename R>
+struct PK;
+
+template <>
+struct PK<float> {
+  using V = float2;
+  static __device__ __forceinline__ V add(V a, V b) { return __fadd2_rn(a, b); }
+  static __device__ __forceinline__ V sub(V a, V b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+  // (a.x b.x - a.y b.y, a.x b.y + a.y b.x) = a.x * b + (-(a.y b.y), a.y b.x)
+  static __device__ __forceinline__ V mul(V a, V b) {
+    const V s = __fmul2_rn(make_float2(a.y, a.y), make_float2(b.y, b.x));
+    return __ffma2_rn(make_float2(a.x, a.x), b, make_float2(-s.x, s.y));
+  }
+  static __device__ __forceinline__ V scale(V a, float s) { return __fmul2_rn(a, make_float2(s, s)); }
+  static __device__ __forceinline__ V conj(V a) { return make_float2(a.x, -a.y); }
+};
+
+template <>
+struct PK<double> {
+  using V = double2;
+  static __device__ __forceinline__ V add(V a, V b) { return make_double2(a.x + b.x, a.y + b.y); }
+  static __device__ __forceinline__ V sub(V a, V b) { return make_double2(a.x - b.x, a.y - b.y); }
+  static __device__ __forceinline__ V mul(V a, V b) {
+    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+  }
+  static __device__ __forceinline__ V scale(V a, double s) { return make_double2(a.x * s, a.y * s); }
+  static __device__ __forceinline__ V conj(V a) { return make_double2(a.x, -a.y); }
+};
+
 // 2x2 complex matrix in the precision of the state
 template <typename R>
 struct Mat2 {
