@@ -84,6 +84,11 @@ int sk_download(const sk_state* s, double* host_c128, int64_t n);
  * pinned-buffer end-to-end copies. */
 int sk_upload_native(sk_state* s, const void* host, int64_t n);
 int sk_download_native(const sk_state* s, void* host, int64_t n);
+/* Stream-ordered download into pinned host memory that returns without
+ * waiting (the data is valid after sk_synchronize or a later synchronising
+ * call on the same stream): lets a caller overlap step k's device->host
+ * copy with step k+1's host->device copy and compute on another stream. */
+int sk_download_native_async(const sk_state* s, void* host, int64_t n);
 
 /* Device-to-device copies from/to a caller-owned buffer of n native
  * elements (torch / NCCL interop); stream-ordered. */

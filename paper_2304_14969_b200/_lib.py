@@ -59,6 +59,7 @@ _SIGS = {
     "sk_download": [p_state, dptr, C.c_int64],
     "sk_upload_native": [p_state, C.c_void_p, C.c_int64],
     "sk_download_native": [p_state, C.c_void_p, C.c_int64],
+    "sk_download_native_async": [p_state, C.c_void_p, C.c_int64],
     "sk_copy_from_device": [p_state, C.c_uint64, C.c_int64],
     "sk_copy_to_device": [p_state, C.c_uint64, C.c_int64],
     "sk_apply_1q": [p_state, C.c_int, dptr],

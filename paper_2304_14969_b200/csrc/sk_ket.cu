@@ -780,6 +780,15 @@ int sk_download_native(const sk_state* s, void* host, int64_t n) {
   return SK_OK;
 }
 
+int sk_download_native_async(const sk_state* s, void* host, int64_t n) {
+  SK_TRY(check_state(s));
+  if (n != s->n) return set_error(SK_EVALUE, "need %lld amplitudes, got %lld", (long long)s->n, (long long)n);
+  DevCtx* c;
+  SK_TRY(ctx_get(s->device, &c));
+  SK_CUDA(cudaMemcpyAsync(host, s->d, (size_t)n * s->elem, cudaMemcpyDeviceToHost, c->stream));
+  return SK_OK;
+}
+
 int sk_copy_from_device(sk_state* s, uint64_t src, int64_t n) {
   SK_TRY(check_state(s));
   if (n != s->n) return set_error(SK_EVALUE, "need %lld amplitudes, got %lld", (long long)s->n, (long long)n);
