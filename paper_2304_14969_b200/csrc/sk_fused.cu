@@ -544,17 +544,21 @@ constexpr int kQRuns = 4;
 struct QStage {
   int code;  // L * 8 + TOP of the stage's chunk; 0 = no chunk (store stage)
   uint32_t flags;
-  int lo, ng, nl, pad;
+  int lo, pad;
   uint64_t tmask, tval, qmask;
   double scale;
-  Run grun[kQRuns], lrun[kQRuns];
   uint64_t reg_goff[kMaxR];
   uint32_t reg_soff[kMaxR];
 };
 
+// Per-thread index parts are precomputed on the host (thr table, one uint4
+// per stage and thread: global index bits lo/hi, swizzled shared-memory
+// byte offset): one L1-resident 16-byte load per thread and stage instead of
+// a bit-deposit.
 struct QSweep {
-  int ntile, nstages, nb, pad;
+  int ntile, nstages, nb, nthreads;
   Run brun[kQRuns];
+  const uint4* thr;  // [nstages][nthreads]
   QStage st[kMaxS];
 };
 
@@ -563,14 +567,6 @@ __device__ __forceinline__ uint64_t deposit_q(uint64_t x, const Run* r, int n) {
 #pragma unroll
   for (int i = 0; i < kQRuns; ++i)
     if (i < n) o |= ((x >> r[i].src) & ((1ull << r[i].w) - 1)) << r[i].dst;
-  return o;
-}
-
-__device__ __forceinline__ uint32_t deposit_q32(uint32_t x, const Run* r, int n) {
-  uint32_t o = 0;
-#pragma unroll
-  for (int i = 0; i < kQRuns; ++i)
-    if (i < n) o |= ((x >> r[i].src) & ((1u << r[i].w) - 1)) << r[i].dst;
   return o;
 }
 
@@ -668,20 +664,20 @@ __device__ __forceinline__ void pk_chunk(const QStage& st, vec2_t<R> (&a)[1 << N
 template <typename R>
 constexpr int qft_max_threads() { return sizeof(R) == 4 ? 512 : 256; }
 
-template <typename R, int NR>
+template <typename R, int NR, int NS>
 __global__ void __launch_bounds__(qft_max_threads<R>(), 2) k_qft(vec2_t<R>* __restrict__ amps, const __grid_constant__ QSweep sw) {
   using V = vec2_t<R>;
   extern __shared__ __align__(16) unsigned char smraw[];
   constexpr int NE = 1 << NR;
-  constexpr int SB = sizeof(V) == 8 ? 4 : 3;
   const uint32_t tid = threadIdx.x;
   const uint64_t base = deposit_q(blockIdx.x, sw.brun, sw.nb);
 
   V a[NE];
-  const int ns = sw.nstages;
-  for (int s = 0; s < ns; ++s) {
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {  // compile-time stages: every st.* is a constant-bank operand
     const QStage& st = sw.st[s];
-    const uint64_t gthr = base | deposit_q(tid, st.grun, st.ng);
+    const uint4 t = __ldg(sw.thr + s * sw.nthreads + tid);
+    const uint64_t gthr = base | ((uint64_t)t.y << 32 | t.x);
     if (s == 0) {
       const char* p = reinterpret_cast<const char*>(amps + gthr);
 #pragma unroll
@@ -695,7 +691,7 @@ __global__ void __launch_bounds__(qft_max_threads<R>(), 2) k_qft(vec2_t<R>* __re
       }
     } else {
       __syncthreads();
-      uint32_t so = swz<SB>(deposit_q32(tid, st.lrun, st.nl)) * (uint32_t)sizeof(V);
+      uint32_t so = t.z;
 #pragma unroll
       for (int k = 0; k < NE; ++k) {
         const int e = k ^ (k >> 1);
@@ -713,7 +709,7 @@ __global__ void __launch_bounds__(qft_max_threads<R>(), 2) k_qft(vec2_t<R>* __re
 #undef SK_QC
       default: break;
     }
-    if (s == ns - 1) {
+    if (s == NS - 1) {
       char* p = reinterpret_cast<char*>(amps + gthr);
 #pragma unroll
       for (int k = 0; k < NE; ++k) {
@@ -726,7 +722,7 @@ __global__ void __launch_bounds__(qft_max_threads<R>(), 2) k_qft(vec2_t<R>* __re
       }
     } else {
       if (s > 0) __syncthreads();
-      uint32_t so = swz<SB>(deposit_q32(tid, st.lrun, st.nl)) * (uint32_t)sizeof(V);
+      uint32_t so = t.z;
 #pragma unroll
       for (int k = 0; k < NE; ++k) {
         const int e = k ^ (k >> 1);
@@ -736,6 +732,7 @@ __global__ void __launch_bounds__(qft_max_threads<R>(), 2) k_qft(vec2_t<R>* __re
     }
   }
 }
+constexpr int kQftMaxStages = 6;
 
 // register bits per stage: 16 fp32 amplitudes (32 regs) or 8 fp64 (32 regs)
 constexpr int kNR32 = 4;
@@ -1039,26 +1036,38 @@ static void pack_kops(std::vector<HostKOp>& h, std::vector<unsigned char>& buf, 
   }
 }
 
-// QSweep for k_qft from a lowered QFT-only sweep: at most one K_QFTS op per
-// stage and at most kQRuns bit runs per mapping; false = keep k_sweep
-static bool qsweep_from(const DSweep& d, const std::vector<HostKOp>& kops, QSweep* q) {
+static uint64_t deposit_h(uint64_t x, const Run* r, int n) {
+  uint64_t o = 0;
+  for (int i = 0; i < n; ++i) o |= ((x >> r[i].src) & ((1ull << r[i].w) - 1)) << r[i].dst;
+  return o;
+}
+
+// QSweep for k_qft from a lowered QFT-only sweep (at most one K_QFTS op per
+// stage), plus its per-thread table appended to `thr`; false = keep k_sweep
+static bool qsweep_from(const DSweep& d, const std::vector<HostKOp>& kops, int NR, size_t esz, QSweep* q,
+                        std::vector<uint4>& thr, size_t* thr_off) {
   *q = QSweep{};
-  if (!d.qft_only || d.nb > kQRuns) return false;
+  if (!d.qft_only || d.nb > kQRuns || d.nstages > kQftMaxStages) return false;
+  const int nthreads = 1 << (d.ntile - NR);
   q->ntile = d.ntile;
   q->nstages = d.nstages;
   q->nb = d.nb;
+  q->nthreads = nthreads;
   for (int i = 0; i < d.nb; ++i) q->brun[i] = d.brun[i];
+  *thr_off = thr.size();
   for (int s = 0; s < d.nstages; ++s) {
     const DStage& a = d.st[s];
     QStage& b = q->st[s];
-    if (a.ng > kQRuns || a.nl > kQRuns || a.op_end - a.op_begin > 1) return false;
-    b.ng = a.ng;
-    b.nl = a.nl;
-    for (int i = 0; i < a.ng; ++i) b.grun[i] = a.grun[i];
-    for (int i = 0; i < a.nl; ++i) b.lrun[i] = a.lrun[i];
+    if (a.op_end - a.op_begin > 1) return false;
     for (int p = 0; p < kMaxR; ++p) {
       b.reg_goff[p] = a.reg_goff[p];
       b.reg_soff[p] = a.reg_soff[p];
+    }
+    for (int t = 0; t < nthreads; ++t) {
+      const uint64_t g = deposit_h((uint64_t)t, a.grun, a.ng);
+      const uint32_t l = (uint32_t)deposit_h((uint64_t)t, a.lrun, a.nl);
+      const uint32_t so = (esz == 8 ? swz<4>(l) : swz<3>(l)) * (uint32_t)esz;
+      thr.push_back(make_uint4((uint32_t)g, (uint32_t)(g >> 32), so, 0u));
     }
     b.code = 0;
     if (a.op_end > a.op_begin) {
@@ -1086,6 +1095,7 @@ struct sk_program {
   std::vector<sk::DSweep> sweeps;
   std::vector<sk::QSweep> qsweeps;  // per sweep: k_qft arguments (valid when qft_ok[i])
   std::vector<char> qft_ok;
+  void* d_thr = nullptr;  // k_qft per-thread tables
   void* d_ops = nullptr;
   int nkops = 0;
 };
@@ -1107,7 +1117,12 @@ static int launch_sweeps(sk_state* s, const sk_program* p, int first, int count,
   if (!attr_set[s->device]) {
     SK_CUDA(cudaFuncSetAttribute(k_sweep<R, NR, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     SK_CUDA(cudaFuncSetAttribute(k_sweep<R, NR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-    SK_CUDA(cudaFuncSetAttribute(k_qft<R, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    SK_CUDA(cudaFuncSetAttribute(k_qft<R, NR, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    SK_CUDA(cudaFuncSetAttribute(k_qft<R, NR, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    SK_CUDA(cudaFuncSetAttribute(k_qft<R, NR, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    SK_CUDA(cudaFuncSetAttribute(k_qft<R, NR, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    SK_CUDA(cudaFuncSetAttribute(k_qft<R, NR, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    SK_CUDA(cudaFuncSetAttribute(k_qft<R, NR, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     attr_set[s->device] = true;
   }
   for (int i = first; i < first + count; ++i) {
@@ -1117,9 +1132,18 @@ static int launch_sweeps(sk_state* s, const sk_program* p, int first, int count,
     const unsigned threads = 1u << (T - NR);
     const size_t smem = ((size_t)1 << T) * sizeof(vec2_t<R>);
     if (tiles > 0x7fffffffull) return set_error(SK_EVALUE, "too many tiles (%d bits outside the tile)", s->width - T);
-    if (p->qft_ok[i] && threads <= (unsigned)qft_max_threads<R>() && use_qft_kernel())
-      k_qft<R, NR><<<(unsigned)tiles, threads, smem, c->stream>>>((vec2_t<R>*)s->d, p->qsweeps[i]);
-    else if (d.qft_only)
+    if (p->qft_ok[i] && threads <= (unsigned)qft_max_threads<R>() && use_qft_kernel()) {
+      const QSweep& q = p->qsweeps[i];
+      vec2_t<R>* d_amps = (vec2_t<R>*)s->d;
+      switch (q.nstages) {
+        case 1: k_qft<R, NR, 1><<<(unsigned)tiles, threads, smem, c->stream>>>(d_amps, q); break;
+        case 2: k_qft<R, NR, 2><<<(unsigned)tiles, threads, smem, c->stream>>>(d_amps, q); break;
+        case 3: k_qft<R, NR, 3><<<(unsigned)tiles, threads, smem, c->stream>>>(d_amps, q); break;
+        case 4: k_qft<R, NR, 4><<<(unsigned)tiles, threads, smem, c->stream>>>(d_amps, q); break;
+        case 5: k_qft<R, NR, 5><<<(unsigned)tiles, threads, smem, c->stream>>>(d_amps, q); break;
+        default: k_qft<R, NR, 6><<<(unsigned)tiles, threads, smem, c->stream>>>(d_amps, q); break;
+      }
+    } else if (d.qft_only)
       k_sweep<R, NR, true><<<(unsigned)tiles, threads, smem, c->stream>>>((vec2_t<R>*)s->d, d, (const KOp<R>*)p->d_ops);
     else
       k_sweep<R, NR, false><<<(unsigned)tiles, threads, smem, c->stream>>>((vec2_t<R>*)s->d, d, (const KOp<R>*)p->d_ops);
@@ -1242,7 +1266,21 @@ int sk_program_create(int width, int dtype, int device, const sk_sweep* sweeps, 
   prog->nr = NR;
   prog->qsweeps.resize(dsw.size());
   prog->qft_ok.resize(dsw.size());
-  for (size_t i = 0; i < dsw.size(); ++i) prog->qft_ok[i] = qsweep_from(dsw[i], kops, &prog->qsweeps[i]);
+  std::vector<uint4> thr;
+  std::vector<size_t> thr_off(dsw.size(), 0);
+  for (size_t i = 0; i < dsw.size(); ++i)
+    prog->qft_ok[i] = qsweep_from(dsw[i], kops, NR, dtype == SK_C64 ? 8 : 16, &prog->qsweeps[i], thr, &thr_off[i]);
+  if (!thr.empty()) {
+    cudaError_t e = cudaMalloc(&prog->d_thr, thr.size() * sizeof(uint4));
+    if (e == cudaSuccess) e = cudaMemcpy(prog->d_thr, thr.data(), thr.size() * sizeof(uint4), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      if (prog->d_thr) cudaFree(prog->d_thr);
+      delete prog;
+      return set_error(SK_ECUDA, "program upload: %s", cudaGetErrorString(e));
+    }
+    for (size_t i = 0; i < dsw.size(); ++i) prog->qsweeps[i].thr = (const uint4*)prog->d_thr + thr_off[i];
+  }
   prog->sweeps = std::move(dsw);
   prog->nkops = (int)kops.size();
   if (!buf.empty()) {
@@ -1251,6 +1289,7 @@ int sk_program_create(int width, int dtype, int device, const sk_sweep* sweeps, 
     if (e != cudaSuccess) {
       cudaGetLastError();
       if (prog->d_ops) cudaFree(prog->d_ops);
+      if (prog->d_thr) cudaFree(prog->d_thr);
       delete prog;
       return set_error(SK_ECUDA, "program upload: %s", cudaGetErrorString(e));
     }
@@ -1287,11 +1326,12 @@ int sk_program_lower(int width, int dtype, const sk_sweep* sweeps, int nsweeps, 
 
 int sk_program_destroy(sk_program* p) {
   if (!p) return SK_OK;
-  if (p->d_ops) {
+  if (p->d_ops || p->d_thr) {
     DevCtx* c;
     SK_TRY(ctx_get(p->device, &c));
     SK_CUDA(cudaStreamSynchronize(c->stream));
-    SK_CUDA(cudaFree(p->d_ops));
+    if (p->d_ops) SK_CUDA(cudaFree(p->d_ops));
+    if (p->d_thr) SK_CUDA(cudaFree(p->d_thr));
   }
   delete p;
   return SK_OK;

@@ -1,6 +1,6 @@
 """Summarise gpurun_out/ ncu artefacts into profiles/ (tracked):
   profiles/<tag>_launches.csv      per-launch device times (ncu launch list)
-  profiles/<tag>_k_sweep.txt       full-set metrics of the k_sweep launches
+  profiles/<tag>_k_qft.txt       full-set metrics of the k_qft launches
   profiles/ncu_summary.json        DRAM bytes per sweep launch (bench.py `traffic`)
 usage: python scripts/make_profile_summary.py <tag> [prof.ncu-rep] [launches.csv] [bench.json]"""
 import csv
@@ -44,7 +44,7 @@ for r in rows[2:]:
     rd = float(r[h.index("dram__bytes_read.sum")]) * (1e9 if units[h.index("dram__bytes_read.sum")] == "Gbyte" else 1e6)
     wr = float(r[h.index("dram__bytes_write.sum")]) * (1e9 if units[h.index("dram__bytes_write.sum")] == "Gbyte" else 1e6)
     dram.append(rd + wr)
-(out / f"{tag}_k_sweep.txt").write_text("\n".join(lines) + "\n")
+(out / f"{tag}_k_qft.txt").write_text("\n".join(lines) + "\n")
 summary = {"tag": tag, "source": str(rep.name), "dram_bytes_per_sweep": sum(dram) / len(dram),
            "dram_bytes_per_launch": dram}
 if bench.exists():
@@ -57,5 +57,5 @@ if bench.exists():
 (out / "ncu_summary.json").write_text(json.dumps(summary, indent=1) + "\n")
 if launches.exists():
     shutil.copy(launches, out / f"{tag}_launches.csv")
-print((out / f"{tag}_k_sweep.txt").read_text())
+print((out / f"{tag}_k_qft.txt").read_text())
 print(json.dumps(summary, indent=1))
