@@ -243,7 +243,7 @@ def run_ours(args, rank: int, world: int):
     host_in = [torch.empty(2 << n_local, dtype=real, pin_memory=True) for _ in range(2)]
     for h in host_in:
         h.copy_(sq.state)
-    host_out = [torch.empty_like(host_in[0]) for _ in range(2)]
+    host_out = [torch.empty(2 << n_local, dtype=real, pin_memory=True) for _ in range(2)]
     pipelined = world == 1
     slabs = [sq.state, torch.empty_like(sq.state)] if pipelined else [sq.state]
     streams = [stream, torch.cuda.Stream(device=dev)] if pipelined else [stream]
