@@ -83,6 +83,7 @@ struct alignas(16) KOp {
   uint64_t fmask;        // phase field mask (applied after >> lo)
   uint64_t pad2;
   R m[8];                // K_MAT: 2x2; K_PHASE: c0 = m[0..1], c1 = m[2..3]; K_BFLY: c0 = m[0..1], c1 = m[4..5]
+  R mr[8];               // m rotated by i per complex entry, (-im, re): packed-FMA operand pairs
   R tw[16];              // K_BFLY (F_TABLE): extra row-1 twiddle per pair k (8 complex)
 };
 
@@ -134,61 +135,74 @@ struct PairMask {
   }
 };
 
-template <typename R, int NR, int P>
-__device__ __forceinline__ void mat_slot(vec2_t<R> (&a)[1 << NR], const Mat2<R>& m, uint32_t emask) {
-  if (emask == PairMask<NR, P>::value()) {
-#pragma unroll
-    for (int e = 0; e < (1 << NR); ++e) {
-      if ((e >> P) & 1) continue;
-      const int e1 = e | (1 << P);
-      vec2_t<R> y0 = cmad2<R>(m.m00, a[e], m.m01, a[e1]);
-      vec2_t<R> y1 = cmad2<R>(m.m10, a[e], m.m11, a[e1]);
-      a[e] = y0;
-      a[e1] = y1;
-    }
+// y = m0 * a0 + m1 * a1 with r = m rotated by i: one paired multiply and
+// three paired FMAs (scalar-broadcast operands are free modifiers)
+template <typename R>
+__device__ __forceinline__ vec2_t<R> cmac2(vec2_t<R> a0, vec2_t<R> a1, vec2_t<R> m0, vec2_t<R> r0, vec2_t<R> m1,
+                                           vec2_t<R> r1) {
+  if constexpr (sizeof(R) == 4) {
+    float2 t = __fmul2_rn(make_float2(a0.x, a0.x), m0);
+    t = __ffma2_rn(make_float2(a0.y, a0.y), r0, t);
+    t = __ffma2_rn(make_float2(a1.x, a1.x), m1, t);
+    return __ffma2_rn(make_float2(a1.y, a1.y), r1, t);
   } else {
+    return mk<R>(a0.x * m0.x + a0.y * r0.x + a1.x * m1.x + a1.y * r1.x,
+                 a0.x * m0.y + a0.y * r0.y + a1.x * m1.y + a1.y * r1.y);
+  }
+}
+
+// c[0..7] = m00, r00, m01, r01, m10, r10, m11, r11
+template <typename R, int NR, int P>
+__device__ __forceinline__ void mat_slot(vec2_t<R> (&a)[1 << NR], const vec2_t<R> (&c)[8], uint32_t emask) {
+  const bool full = emask == PairMask<NR, P>::value();
 #pragma unroll
-    for (int e = 0; e < (1 << NR); ++e) {
-      if ((e >> P) & 1) continue;
-      if (!((emask >> e) & 1u)) continue;
-      const int e1 = e | (1 << P);
-      vec2_t<R> y0 = cmad2<R>(m.m00, a[e], m.m01, a[e1]);
-      vec2_t<R> y1 = cmad2<R>(m.m10, a[e], m.m11, a[e1]);
-      a[e] = y0;
-      a[e1] = y1;
-    }
+  for (int e = 0; e < (1 << NR); ++e) {
+    if ((e >> P) & 1) continue;
+    if (!full && !((emask >> e) & 1u)) continue;
+    const int e1 = e | (1 << P);
+    const vec2_t<R> y0 = cmac2<R>(a[e], a[e1], c[0], c[1], c[2], c[3]);
+    const vec2_t<R> y1 = cmac2<R>(a[e], a[e1], c[4], c[5], c[6], c[7]);
+    a[e] = y0;
+    a[e1] = y1;
   }
 }
 
 template <typename R, int NR, int P>
 __device__ __forceinline__ void matr_slot(vec2_t<R> (&a)[1 << NR], R m00, R m01, R m10, R m11, uint32_t emask) {
+  const bool full = emask == PairMask<NR, P>::value();
 #pragma unroll
   for (int e = 0; e < (1 << NR); ++e) {
     if ((e >> P) & 1) continue;
-    if (!((emask >> e) & 1u)) continue;
+    if (!full && !((emask >> e) & 1u)) continue;
     const int e1 = e | (1 << P);
     const vec2_t<R> x0 = a[e], x1 = a[e1];
-    a[e] = mk<R>(m00 * x0.x + m01 * x1.x, m00 * x0.y + m01 * x1.y);
-    a[e1] = mk<R>(m10 * x0.x + m11 * x1.x, m10 * x0.y + m11 * x1.y);
+    if constexpr (sizeof(R) == 4) {
+      a[e] = __ffma2_rn(x1, make_float2(m01, m01), __fmul2_rn(x0, make_float2(m00, m00)));
+      a[e1] = __ffma2_rn(x1, make_float2(m11, m11), __fmul2_rn(x0, make_float2(m10, m10)));
+    } else {
+      a[e] = mk<R>(m00 * x0.x + m01 * x1.x, m00 * x0.y + m01 * x1.y);
+      a[e1] = mk<R>(m10 * x0.x + m11 * x1.x, m10 * x0.y + m11 * x1.y);
+    }
   }
 }
 
 template <typename R, int NR, int P>
 __device__ __forceinline__ void bfly_slot(vec2_t<R> (&a)[1 << NR], vec2_t<R> c0, const vec2_t<R>* w, unsigned flags) {
   // pair k of slot P: e = k with a zero inserted at bit P, e1 = e | 2^P
+  using PK_ = PK<R>;
 #pragma unroll
   for (int e = 0, k = 0; e < (1 << NR); ++e) {
     if ((e >> P) & 1) continue;
     const int e1 = e | (1 << P);
-    const vec2_t<R> s = mk<R>(a[e].x + a[e1].x, a[e].y + a[e1].y);
-    const vec2_t<R> d = mk<R>(a[e].x - a[e1].x, a[e].y - a[e1].y);
+    const vec2_t<R> s = PK_::add(a[e], a[e1]);
+    const vec2_t<R> d = PK_::sub(a[e], a[e1]);
     if (flags & F_C0ONE)
       a[e] = s;
     else if (flags & F_C0REAL)
-      a[e] = mk<R>(c0.x * s.x, c0.x * s.y);
+      a[e] = PK_::scale(s, c0.x);
     else
-      a[e] = cmul<R>(c0, s);
-    a[e1] = cmul<R>(w[k], d);
+      a[e] = PK_::mul(c0, s);
+    a[e1] = PK_::mul(w[k], d);
     ++k;
   }
 }
@@ -204,7 +218,7 @@ __device__ __forceinline__ void phase_pat(vec2_t<R> (&a)[1 << NR], vec2_t<R> c) 
   if constexpr (P < NR && Q < NR) {
 #pragma unroll
     for (int e = 0; e < (1 << NR); ++e)
-      if (pat_hit<NR, P, VP, Q, VQ>(e)) a[e] = cmul<R>(a[e], c);
+      if (pat_hit<NR, P, VP, Q, VQ>(e)) a[e] = PK<R>::mul(a[e], c);
   }
 }
 
@@ -413,11 +427,11 @@ __device__ __forceinline__ void apply_kop(const KOp<R>* __restrict__ op, vec2_t<
   if (kind == K_BFLY) {
     const vec2_t<R> c0 = mk<R>(op->m[0], op->m[1]);
     vec2_t<R> c1 = mk<R>(op->m[4], op->m[5]);
-    if (h.flags & F_FOLD) c1 = cmul<R>(c1, thread_phase<R>(op->turn, gthr, h.lo, op->fmask));
+    if (h.flags & F_FOLD) c1 = PK<R>::mul(c1, thread_phase<R>(op->turn, gthr, h.lo, op->fmask));
     vec2_t<R> w[1 << (NR - 1)];
     if (h.flags & F_TABLE) {
 #pragma unroll
-      for (int k = 0; k < (1 << (NR - 1)); ++k) w[k] = cmul<R>(c1, mk<R>(op->tw[2 * k], op->tw[2 * k + 1]));
+      for (int k = 0; k < (1 << (NR - 1)); ++k) w[k] = PK<R>::mul(c1, mk<R>(op->tw[2 * k], op->tw[2 * k + 1]));
     } else {
 #pragma unroll
       for (int k = 0; k < (1 << (NR - 1)); ++k) w[k] = c1;
@@ -435,7 +449,7 @@ __device__ __forceinline__ void apply_kop(const KOp<R>* __restrict__ op, vec2_t<
     if (!phase_dispatch<R, NR>(h.pat, a, c)) {
 #pragma unroll
       for (int e = 0; e < (1 << NR); ++e)
-        if ((emask >> e) & 1u) a[e] = cmul<R>(a[e], c);
+        if ((emask >> e) & 1u) a[e] = PK<R>::mul(a[e], c);
     }
   } else if (kind == K_MATR) {
     const R m00 = op->m[0], m01 = op->m[2], m10 = op->m[4], m11 = op->m[6];
@@ -443,37 +457,45 @@ __device__ __forceinline__ void apply_kop(const KOp<R>* __restrict__ op, vec2_t<
     SK_SLOT_SWITCH(h.slot, SK_MR)
 #undef SK_MR
   } else {  // K_MAT
-    Mat2<R> m;
-    m.m00 = mk<R>(op->m[0], op->m[1]);
-    m.m01 = mk<R>(op->m[2], op->m[3]);
-    m.m10 = mk<R>(op->m[4], op->m[5]);
-    m.m11 = mk<R>(op->m[6], op->m[7]);
+    vec2_t<R> c[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      c[2 * i] = mk<R>(op->m[2 * i], op->m[2 * i + 1]);
+      c[2 * i + 1] = mk<R>(op->mr[2 * i], op->mr[2 * i + 1]);
+    }
     if (h.flags & F_FOLD) {
       const vec2_t<R> tau = thread_phase<R>(op->turn, gthr, h.lo, op->fmask);
-      m.m10 = cmul<R>(m.m10, tau);
-      m.m11 = cmul<R>(m.m11, tau);
+      c[4] = PK<R>::mul(c[4], tau);
+      c[6] = PK<R>::mul(c[6], tau);
+      c[5] = mk<R>(-c[4].y, c[4].x);
+      c[7] = mk<R>(-c[6].y, c[6].x);
     }
-#define SK_M(P) mat_slot<R, NR, P>(a, m, emask)
+#define SK_M(P) mat_slot<R, NR, P>(a, c, emask)
     SK_SLOT_SWITCH(h.slot, SK_M)
 #undef SK_M
   }
 }
 
-template <typename R, int NR, bool QFTONLY>
-__global__ void __launch_bounds__(512, 2) k_sweep(vec2_t<R>* __restrict__ amps, const __grid_constant__ DSweep sw,
-                                                  const KOp<R>* __restrict__ ops) {
+// Generic fused sweep (random circuits, mixed gate streams): NS compile-time
+// stages with per-thread index parts from the host-built table `thr`
+// (uint4 per stage and thread: global bits lo/hi, swizzled shared offset),
+// ops interpreted from `ops` with warp-uniform loads and packed arithmetic.
+template <typename R, int NR, int NS>
+__global__ void __launch_bounds__(512, 1) k_sweep(vec2_t<R>* __restrict__ amps, const __grid_constant__ DSweep sw,
+                                                  const KOp<R>* __restrict__ ops, const uint4* __restrict__ thr) {
   using V = vec2_t<R>;
   extern __shared__ __align__(16) unsigned char smraw[];
   constexpr int NE = 1 << NR;
-  constexpr int SB = sizeof(V) == 8 ? 4 : 3;
   const uint32_t tid = threadIdx.x;
   const uint64_t base = deposit(blockIdx.x, sw.brun, sw.nb);
+  const int nthreads = blockDim.x;
 
   V a[NE];
-  const int ns = sw.nstages;
-  for (int s = 0; s < ns; ++s) {
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
     const DStage& st = sw.st[s];
-    const uint64_t gthr = base | deposit(tid, st.grun, st.ng);
+    const uint4 t = __ldg(thr + s * nthreads + tid);
+    const uint64_t gthr = base | ((uint64_t)t.y << 32 | t.x);
     if (s == 0) {
       const char* p = reinterpret_cast<const char*>(amps + gthr);
 #pragma unroll
@@ -487,7 +509,7 @@ __global__ void __launch_bounds__(512, 2) k_sweep(vec2_t<R>* __restrict__ amps, 
       }
     } else {
       __syncthreads();
-      uint32_t so = swz<SB>((uint32_t)deposit(tid, st.lrun, st.nl)) * (uint32_t)sizeof(V);
+      uint32_t so = t.z;
 #pragma unroll
       for (int k = 0; k < NE; ++k) {
         const int e = k ^ (k >> 1);
@@ -495,17 +517,8 @@ __global__ void __launch_bounds__(512, 2) k_sweep(vec2_t<R>* __restrict__ amps, 
         a[e] = *reinterpret_cast<const V*>(smraw + so);
       }
     }
-    if (QFTONLY) {
-      for (int o = st.op_begin; o < st.op_end; ++o) {
-        const uint4 raw = *reinterpret_cast<const uint4*>(&ops[o].h);
-        KHdr h;
-        memcpy(&h, &raw, sizeof(h));
-        qft_dispatch<R, NR>(ops + o, h, a, gthr);
-      }
-    } else {
-      for (int o = st.op_begin; o < st.op_end; ++o) apply_kop<R, NR>(ops + o, a, gthr);
-    }
-    if (s == ns - 1) {
+    for (int o = st.op_begin; o < st.op_end; ++o) apply_kop<R, NR>(ops + o, a, gthr);
+    if (s == NS - 1) {
       char* p = reinterpret_cast<char*>(amps + gthr);
 #pragma unroll
       for (int k = 0; k < NE; ++k) {
@@ -518,7 +531,7 @@ __global__ void __launch_bounds__(512, 2) k_sweep(vec2_t<R>* __restrict__ amps, 
       }
     } else {
       if (s > 0) __syncthreads();
-      uint32_t so = swz<SB>((uint32_t)deposit(tid, st.lrun, st.nl)) * (uint32_t)sizeof(V);
+      uint32_t so = t.z;
 #pragma unroll
       for (int k = 0; k < NE; ++k) {
         const int e = k ^ (k >> 1);
@@ -1031,6 +1044,10 @@ static void pack_kops(std::vector<HostKOp>& h, std::vector<unsigned char>& buf, 
     x.turn = h[i].turn;
     x.fmask = h[i].fmask;
     for (int j = 0; j < 8; ++j) x.m[j] = (R)h[i].m[j];
+    for (int j = 0; j < 4; ++j) {
+      x.mr[2 * j] = (R)-h[i].m[2 * j + 1];
+      x.mr[2 * j + 1] = (R)h[i].m[2 * j];
+    }
     for (int j = 0; j < 16; ++j) x.tw[j] = (R)h[i].tw[j];
     k[i] = x;
   }
@@ -1042,19 +1059,31 @@ static uint64_t deposit_h(uint64_t x, const Run* r, int n) {
   return o;
 }
 
+// per-thread index table of a sweep: [stage][thread] = {global bits lo, hi,
+// swizzled shared-memory byte offset, 0}
+static void append_thr(const DSweep& d, int NR, size_t esz, std::vector<uint4>& thr) {
+  const int nthreads = 1 << (d.ntile - NR);
+  for (int s = 0; s < d.nstages; ++s) {
+    const DStage& a = d.st[s];
+    for (int t = 0; t < nthreads; ++t) {
+      const uint64_t g = deposit_h((uint64_t)t, a.grun, a.ng);
+      const uint32_t l = (uint32_t)deposit_h((uint64_t)t, a.lrun, a.nl);
+      const uint32_t so = (esz == 8 ? swz<4>(l) : swz<3>(l)) * (uint32_t)esz;
+      thr.push_back(make_uint4((uint32_t)g, (uint32_t)(g >> 32), so, 0u));
+    }
+  }
+}
+
 // QSweep for k_qft from a lowered QFT-only sweep (at most one K_QFTS op per
-// stage), plus its per-thread table appended to `thr`; false = keep k_sweep
-static bool qsweep_from(const DSweep& d, const std::vector<HostKOp>& kops, int NR, size_t esz, QSweep* q,
-                        std::vector<uint4>& thr, size_t* thr_off) {
+// stage); false = run it through the generic k_sweep
+static bool qsweep_from(const DSweep& d, const std::vector<HostKOp>& kops, int NR, QSweep* q) {
   *q = QSweep{};
   if (!d.qft_only || d.nb > kQRuns || d.nstages > kQftMaxStages) return false;
-  const int nthreads = 1 << (d.ntile - NR);
   q->ntile = d.ntile;
   q->nstages = d.nstages;
   q->nb = d.nb;
-  q->nthreads = nthreads;
+  q->nthreads = 1 << (d.ntile - NR);
   for (int i = 0; i < d.nb; ++i) q->brun[i] = d.brun[i];
-  *thr_off = thr.size();
   for (int s = 0; s < d.nstages; ++s) {
     const DStage& a = d.st[s];
     QStage& b = q->st[s];
@@ -1062,12 +1091,6 @@ static bool qsweep_from(const DSweep& d, const std::vector<HostKOp>& kops, int N
     for (int p = 0; p < kMaxR; ++p) {
       b.reg_goff[p] = a.reg_goff[p];
       b.reg_soff[p] = a.reg_soff[p];
-    }
-    for (int t = 0; t < nthreads; ++t) {
-      const uint64_t g = deposit_h((uint64_t)t, a.grun, a.ng);
-      const uint32_t l = (uint32_t)deposit_h((uint64_t)t, a.lrun, a.nl);
-      const uint32_t so = (esz == 8 ? swz<4>(l) : swz<3>(l)) * (uint32_t)esz;
-      thr.push_back(make_uint4((uint32_t)g, (uint32_t)(g >> 32), so, 0u));
     }
     b.code = 0;
     if (a.op_end > a.op_begin) {
@@ -1095,7 +1118,8 @@ struct sk_program {
   std::vector<sk::DSweep> sweeps;
   std::vector<sk::QSweep> qsweeps;  // per sweep: k_qft arguments (valid when qft_ok[i])
   std::vector<char> qft_ok;
-  void* d_thr = nullptr;  // k_qft per-thread tables
+  std::vector<size_t> thr_off;  // per sweep: offset of its per-thread table in d_thr (uint4 units)
+  void* d_thr = nullptr;  // per-thread index tables
   void* d_ops = nullptr;
   int nkops = 0;
 };
@@ -1115,8 +1139,14 @@ template <typename R, int NR>
 static int launch_sweeps(sk_state* s, const sk_program* p, int first, int count, DevCtx* c) {
   static bool attr_set[64] = {false};
   if (!attr_set[s->device]) {
-    SK_CUDA(cudaFuncSetAttribute(k_sweep<R, NR, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-    SK_CUDA(cudaFuncSetAttribute(k_sweep<R, NR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    SK_CUDA(cudaFuncSetAttribute(k_sweep<R, NR, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    SK_CUDA(cudaFuncSetAttribute(k_sweep<R, NR, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    SK_CUDA(cudaFuncSetAttribute(k_sweep<R, NR, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    SK_CUDA(cudaFuncSetAttribute(k_sweep<R, NR, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    SK_CUDA(cudaFuncSetAttribute(k_sweep<R, NR, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    SK_CUDA(cudaFuncSetAttribute(k_sweep<R, NR, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    SK_CUDA(cudaFuncSetAttribute(k_sweep<R, NR, 7>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    SK_CUDA(cudaFuncSetAttribute(k_sweep<R, NR, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     SK_CUDA(cudaFuncSetAttribute(k_qft<R, NR, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     SK_CUDA(cudaFuncSetAttribute(k_qft<R, NR, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     SK_CUDA(cudaFuncSetAttribute(k_qft<R, NR, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
@@ -1143,10 +1173,18 @@ static int launch_sweeps(sk_state* s, const sk_program* p, int first, int count,
         case 5: k_qft<R, NR, 5><<<(unsigned)tiles, threads, smem, c->stream>>>(d_amps, q); break;
         default: k_qft<R, NR, 6><<<(unsigned)tiles, threads, smem, c->stream>>>(d_amps, q); break;
       }
-    } else if (d.qft_only)
-      k_sweep<R, NR, true><<<(unsigned)tiles, threads, smem, c->stream>>>((vec2_t<R>*)s->d, d, (const KOp<R>*)p->d_ops);
-    else
-      k_sweep<R, NR, false><<<(unsigned)tiles, threads, smem, c->stream>>>((vec2_t<R>*)s->d, d, (const KOp<R>*)p->d_ops);
+    } else {
+      const KOp<R>* ops = (const KOp<R>*)p->d_ops;
+      const uint4* thr = (const uint4*)p->d_thr + p->thr_off[i];
+      vec2_t<R>* d_amps = (vec2_t<R>*)s->d;
+      switch (d.nstages) {
+#define SK_GS(NS_) \
+  case NS_: k_sweep<R, NR, NS_><<<(unsigned)tiles, threads, smem, c->stream>>>(d_amps, d, ops, thr); break;
+        SK_GS(1) SK_GS(2) SK_GS(3) SK_GS(4) SK_GS(5) SK_GS(6) SK_GS(7) SK_GS(8)
+#undef SK_GS
+        default: return set_error(SK_EVALUE, "sweep %d: %d stages", i, d.nstages);
+      }
+    }
     SK_CHECK_LAUNCH();
   }
   return SK_OK;
@@ -1267,9 +1305,12 @@ int sk_program_create(int width, int dtype, int device, const sk_sweep* sweeps, 
   prog->qsweeps.resize(dsw.size());
   prog->qft_ok.resize(dsw.size());
   std::vector<uint4> thr;
-  std::vector<size_t> thr_off(dsw.size(), 0);
-  for (size_t i = 0; i < dsw.size(); ++i)
-    prog->qft_ok[i] = qsweep_from(dsw[i], kops, NR, dtype == SK_C64 ? 8 : 16, &prog->qsweeps[i], thr, &thr_off[i]);
+  prog->thr_off.assign(dsw.size(), 0);
+  for (size_t i = 0; i < dsw.size(); ++i) {
+    prog->thr_off[i] = thr.size();
+    append_thr(dsw[i], NR, dtype == SK_C64 ? 8 : 16, thr);
+    prog->qft_ok[i] = qsweep_from(dsw[i], kops, NR, &prog->qsweeps[i]);
+  }
   if (!thr.empty()) {
     cudaError_t e = cudaMalloc(&prog->d_thr, thr.size() * sizeof(uint4));
     if (e == cudaSuccess) e = cudaMemcpy(prog->d_thr, thr.data(), thr.size() * sizeof(uint4), cudaMemcpyHostToDevice);
@@ -1279,7 +1320,7 @@ int sk_program_create(int width, int dtype, int device, const sk_sweep* sweeps, 
       delete prog;
       return set_error(SK_ECUDA, "program upload: %s", cudaGetErrorString(e));
     }
-    for (size_t i = 0; i < dsw.size(); ++i) prog->qsweeps[i].thr = (const uint4*)prog->d_thr + thr_off[i];
+    for (size_t i = 0; i < dsw.size(); ++i) prog->qsweeps[i].thr = (const uint4*)prog->d_thr + prog->thr_off[i];
   }
   prog->sweeps = std::move(dsw);
   prog->nkops = (int)kops.size();
