@@ -40,10 +40,12 @@ MAX_STAGES = _lib.SK_MAX_STAGES
 
 # kernel geometry per dtype (csrc/sk_fused.cu): register bits, max tile bits,
 # low contiguous bits (256 B per warp access)
-GEOMETRY = {"c64": dict(nreg=4, tile=13, low=5, qft_tile=12, qft_low=4),
-            "c128": dict(nreg=3, tile=12, low=4, qft_tile=10, qft_low=4)}
-# QFT windows use smaller tiles (more CTAs per SM; measured best on B200 by
-# scripts/tune_qft.py: c64 QFT-27 1.57 ms at T=12/low=4 vs 1.74 ms at T=13/low=5)
+GEOMETRY = {"c64": dict(nreg=4, tile=11, low=5, qft_tile=12, qft_low=4),
+            "c128": dict(nreg=3, tile=10, low=4, qft_tile=10, qft_low=4)}
+# Measured on B200 (scripts/tune_qft.py): QFT-27 c64 1.10 ms at T=12/low=4
+# (k_qft); random 30x20 c64 384 ms at T=11/low=5 vs 467 ms at T=13/low=5 and
+# c128 803 ms at T=10/low=4 vs 917 ms at T=12 (generic k_sweep: fewer, larger
+# tiles lose occupancy to its ~110 registers per thread).
 
 
 @dataclass
