@@ -20,7 +20,7 @@ def check_structure(plan: fusion.Plan):
     geo = fusion.GEOMETRY[plan.dtype]
     for sp in plan.sweeps:
         assert sp.tile_bits == sorted(set(sp.tile_bits))
-        assert len(sp.tile_bits) == min(geo["tile"], plan.width) or len(sp.tile_bits) <= geo["tile"]
+        assert len(sp.tile_bits) <= max(geo["tile"], geo["qft_tile"], 13 if plan.dtype == "c64" else 12)
         assert 1 <= len(sp.stages) <= fusion.MAX_STAGES
         for st in sp.stages:
             assert len(st.reg_bits) == plan.nreg == len(set(st.reg_bits))
