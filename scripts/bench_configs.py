@@ -167,7 +167,8 @@ if __name__ == "__main__":
             rand30()
         elif w == "qft34":
             qft34()
-        elif w == "sdrp54":
-            sdrp54()
+        elif w.startswith("sdrp54"):  # sdrp54[:budget_log2[:circuits]]
+            parts = w.split(":")
+            sdrp54(int(parts[1]) if len(parts) > 1 else 31, 7, int(parts[2]) if len(parts) > 2 else 1)
         elif w == "hybrid":
             hybrid()
