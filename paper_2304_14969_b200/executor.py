@@ -56,6 +56,11 @@ class Program:
                              f"state is width {state.width} {state.dtype}")
         _lib.call("sk_program_run", state._h, self._h, first, count)
 
+    def run_handle(self, handle, first: int = 0, count: int = -1) -> None:
+        """Run on a raw sk_state handle (e.g. an sk_wrap view over a torch /
+        NCCL buffer); the C side checks width, dtype and device."""
+        _lib.call("sk_program_run", handle, self._h, first, count)
+
 
 def compile_circuit(circuit: Circuit, dtype: str | None = None, device: int | None = None, **plan_kw) -> Program:
     dtype = dtype or get_default_dtype()
