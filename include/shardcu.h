@@ -186,11 +186,13 @@ typedef struct {
   int32_t nstages;
   int32_t reg_bits[SK_MAX_STAGES][SK_MAX_REG_BITS]; /* global qubits held in registers */
   int32_t op_begin[SK_MAX_STAGES + 1];        /* stage s runs ops[op_begin[s] .. op_begin[s+1]) */
+  int32_t nreg;                               /* register bits per stage: 0 = sk_program_reg_bits default;
+                                                 c64: 4, c128: 3 or 4 (QFT windows use 4) */
 } sk_sweep;
 
-/* Validate and upload a program for an n-qubit state of `dtype`.  `nreg`
- * is the register-bit count the sweeps were planned with (must equal the
- * kernel's: sk_program_reg_bits). */
+/* Validate and upload a program for an n-qubit state of `dtype`.  Each
+ * sweep's `nreg` is the register-bit count it was planned with
+ * (sk_program_reg_bits gives the dtype default). */
 int sk_program_reg_bits(int dtype, int* nreg);
 int sk_program_create(int width, int dtype, int device, const sk_sweep* sweeps, int nsweeps,
                       const sk_op* ops, int nops, sk_program** out);

@@ -34,7 +34,7 @@ class SkOp(C.Structure):
 class SkSweep(C.Structure):
     _fields_ = [("ntile", C.c_int32), ("tile_bits", C.c_int32 * SK_MAX_TILE_BITS), ("nstages", C.c_int32),
                 ("reg_bits", (C.c_int32 * SK_MAX_REG_BITS) * SK_MAX_STAGES),
-                ("op_begin", C.c_int32 * (SK_MAX_STAGES + 1))]
+                ("op_begin", C.c_int32 * (SK_MAX_STAGES + 1)), ("nreg", C.c_int32)]
 
 
 # name -> argtypes (restype is always c_int unless listed in _RESTYPES)

@@ -58,6 +58,7 @@ struct DStage {
 struct DSweep {
   int ntile;
   int nstages;
+  int nr;        // register bits per stage (4 for c64; 3 or 4 for c128)
   int qft_only;  // every kernel op is a K_QFTS chunk: use the specialised kernel
   int nb;
   Run brun[kMaxRuns];  // tile index (blockIdx) bits -> non-tile global bits
@@ -793,6 +794,7 @@ struct HostKOp {
   uint64_t tmask = 0, tval = 0, qmask = 0, turn = 0, fmask = 0;
   double m[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   double tw[16] = {1, 0, 1, 0, 1, 0, 1, 0, 1, 0, 1, 0, 1, 0, 1, 0};
+  int nr = 4;  // register bits of the sweep it belongs to (pattern codes depend on it)
 };
 
 struct StageCtx {
@@ -1025,11 +1027,11 @@ static int lower_op(const StageCtx& c, const sk_op& op, int o, int width, std::v
 }
 
 template <typename R>
-static void pack_kops(std::vector<HostKOp>& h, std::vector<unsigned char>& buf, int NR) {
+static void pack_kops(std::vector<HostKOp>& h, std::vector<unsigned char>& buf) {
   buf.assign(sizeof(KOp<R>) * h.size(), 0);
   KOp<R>* k = reinterpret_cast<KOp<R>*>(buf.data());
   for (size_t i = 0; i < h.size(); ++i) {
-    if (h[i].kind == K_PHASE || h[i].kind == K_TPHASE) h[i].pat = pattern_of(NR, h[i].emask);
+    if (h[i].kind == K_PHASE || h[i].kind == K_TPHASE) h[i].pat = pattern_of(h[i].nr, h[i].emask);
     KOp<R> x{};
     x.h.kind = (int16_t)h[i].kind;
     x.h.slot = (int8_t)h[i].slot;
@@ -1061,8 +1063,8 @@ static uint64_t deposit_h(uint64_t x, const Run* r, int n) {
 
 // per-thread index table of a sweep: [stage][thread] = {global bits lo, hi,
 // swizzled shared-memory byte offset, 0}
-static void append_thr(const DSweep& d, int NR, size_t esz, std::vector<uint4>& thr) {
-  const int nthreads = 1 << (d.ntile - NR);
+static void append_thr(const DSweep& d, size_t esz, std::vector<uint4>& thr) {
+  const int nthreads = 1 << (d.ntile - d.nr);
   for (int s = 0; s < d.nstages; ++s) {
     const DStage& a = d.st[s];
     for (int t = 0; t < nthreads; ++t) {
@@ -1076,13 +1078,13 @@ static void append_thr(const DSweep& d, int NR, size_t esz, std::vector<uint4>& 
 
 // QSweep for k_qft from a lowered QFT-only sweep (at most one K_QFTS op per
 // stage); false = run it through the generic k_sweep
-static bool qsweep_from(const DSweep& d, const std::vector<HostKOp>& kops, int NR, QSweep* q) {
+static bool qsweep_from(const DSweep& d, const std::vector<HostKOp>& kops, QSweep* q) {
   *q = QSweep{};
   if (!d.qft_only || d.nb > kQRuns || d.nstages > kQftMaxStages) return false;
   q->ntile = d.ntile;
   q->nstages = d.nstages;
   q->nb = d.nb;
-  q->nthreads = 1 << (d.ntile - NR);
+  q->nthreads = 1 << (d.ntile - d.nr);
   for (int i = 0; i < d.nb; ++i) q->brun[i] = d.brun[i];
   for (int s = 0; s < d.nstages; ++s) {
     const DStage& a = d.st[s];
@@ -1136,56 +1138,59 @@ static bool use_qft_kernel() {
 }
 
 template <typename R, int NR>
-static int launch_sweeps(sk_state* s, const sk_program* p, int first, int count, DevCtx* c) {
+static int launch_one(sk_state* s, const sk_program* p, int i, DevCtx* c) {
   static bool attr_set[64] = {false};
   if (!attr_set[s->device]) {
-    SK_CUDA(cudaFuncSetAttribute(k_sweep<R, NR, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-    SK_CUDA(cudaFuncSetAttribute(k_sweep<R, NR, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-    SK_CUDA(cudaFuncSetAttribute(k_sweep<R, NR, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-    SK_CUDA(cudaFuncSetAttribute(k_sweep<R, NR, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-    SK_CUDA(cudaFuncSetAttribute(k_sweep<R, NR, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-    SK_CUDA(cudaFuncSetAttribute(k_sweep<R, NR, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-    SK_CUDA(cudaFuncSetAttribute(k_sweep<R, NR, 7>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-    SK_CUDA(cudaFuncSetAttribute(k_sweep<R, NR, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-    SK_CUDA(cudaFuncSetAttribute(k_qft<R, NR, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-    SK_CUDA(cudaFuncSetAttribute(k_qft<R, NR, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-    SK_CUDA(cudaFuncSetAttribute(k_qft<R, NR, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-    SK_CUDA(cudaFuncSetAttribute(k_qft<R, NR, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-    SK_CUDA(cudaFuncSetAttribute(k_qft<R, NR, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-    SK_CUDA(cudaFuncSetAttribute(k_qft<R, NR, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+#define SK_ATTR(K) SK_CUDA(cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024))
+    SK_ATTR((k_sweep<R, NR, 1>)); SK_ATTR((k_sweep<R, NR, 2>)); SK_ATTR((k_sweep<R, NR, 3>));
+    SK_ATTR((k_sweep<R, NR, 4>)); SK_ATTR((k_sweep<R, NR, 5>)); SK_ATTR((k_sweep<R, NR, 6>));
+    SK_ATTR((k_sweep<R, NR, 7>)); SK_ATTR((k_sweep<R, NR, 8>));
+    SK_ATTR((k_qft<R, NR, 1>)); SK_ATTR((k_qft<R, NR, 2>)); SK_ATTR((k_qft<R, NR, 3>));
+    SK_ATTR((k_qft<R, NR, 4>)); SK_ATTR((k_qft<R, NR, 5>)); SK_ATTR((k_qft<R, NR, 6>));
+#undef SK_ATTR
     attr_set[s->device] = true;
   }
-  for (int i = first; i < first + count; ++i) {
-    const DSweep& d = p->sweeps[i];
-    const int T = d.ntile;
-    const uint64_t tiles = 1ull << (s->width - T);
-    const unsigned threads = 1u << (T - NR);
-    const size_t smem = ((size_t)1 << T) * sizeof(vec2_t<R>);
-    if (tiles > 0x7fffffffull) return set_error(SK_EVALUE, "too many tiles (%d bits outside the tile)", s->width - T);
-    if (p->qft_ok[i] && threads <= (unsigned)qft_max_threads<R>() && use_qft_kernel()) {
-      const QSweep& q = p->qsweeps[i];
-      vec2_t<R>* d_amps = (vec2_t<R>*)s->d;
-      switch (q.nstages) {
-        case 1: k_qft<R, NR, 1><<<(unsigned)tiles, threads, smem, c->stream>>>(d_amps, q); break;
-        case 2: k_qft<R, NR, 2><<<(unsigned)tiles, threads, smem, c->stream>>>(d_amps, q); break;
-        case 3: k_qft<R, NR, 3><<<(unsigned)tiles, threads, smem, c->stream>>>(d_amps, q); break;
-        case 4: k_qft<R, NR, 4><<<(unsigned)tiles, threads, smem, c->stream>>>(d_amps, q); break;
-        case 5: k_qft<R, NR, 5><<<(unsigned)tiles, threads, smem, c->stream>>>(d_amps, q); break;
-        default: k_qft<R, NR, 6><<<(unsigned)tiles, threads, smem, c->stream>>>(d_amps, q); break;
-      }
-    } else {
-      const KOp<R>* ops = (const KOp<R>*)p->d_ops;
-      const uint4* thr = (const uint4*)p->d_thr + p->thr_off[i];
-      vec2_t<R>* d_amps = (vec2_t<R>*)s->d;
-      switch (d.nstages) {
+  const DSweep& d = p->sweeps[i];
+  const int T = d.ntile;
+  const uint64_t tiles = 1ull << (s->width - T);
+  const unsigned threads = 1u << (T - NR);
+  const size_t smem = ((size_t)1 << T) * sizeof(vec2_t<R>);
+  if (tiles > 0x7fffffffull) return set_error(SK_EVALUE, "too many tiles (%d bits outside the tile)", s->width - T);
+  vec2_t<R>* d_amps = (vec2_t<R>*)s->d;
+  if (p->qft_ok[i] && threads <= (unsigned)qft_max_threads<R>() && use_qft_kernel()) {
+    const QSweep& q = p->qsweeps[i];
+    switch (q.nstages) {
+#define SK_QS(NS_) \
+  case NS_: k_qft<R, NR, NS_><<<(unsigned)tiles, threads, smem, c->stream>>>(d_amps, q); break;
+      SK_QS(1) SK_QS(2) SK_QS(3) SK_QS(4) SK_QS(5) SK_QS(6)
+#undef SK_QS
+      default: return set_error(SK_EVALUE, "sweep %d: %d stages", i, q.nstages);
+    }
+  } else {
+    const KOp<R>* ops = (const KOp<R>*)p->d_ops;
+    const uint4* thr = (const uint4*)p->d_thr + p->thr_off[i];
+    switch (d.nstages) {
 #define SK_GS(NS_) \
   case NS_: k_sweep<R, NR, NS_><<<(unsigned)tiles, threads, smem, c->stream>>>(d_amps, d, ops, thr); break;
-        SK_GS(1) SK_GS(2) SK_GS(3) SK_GS(4) SK_GS(5) SK_GS(6) SK_GS(7) SK_GS(8)
+      SK_GS(1) SK_GS(2) SK_GS(3) SK_GS(4) SK_GS(5) SK_GS(6) SK_GS(7) SK_GS(8)
 #undef SK_GS
-        default: return set_error(SK_EVALUE, "sweep %d: %d stages", i, d.nstages);
-      }
+      default: return set_error(SK_EVALUE, "sweep %d: %d stages", i, d.nstages);
     }
-    SK_CHECK_LAUNCH();
+  }
+  SK_CHECK_LAUNCH();
+  return SK_OK;
+}
+
+static int launch_sweeps(sk_state* s, const sk_program* p, int first, int count, DevCtx* c) {
+  for (int i = first; i < first + count; ++i) {
+    const int nr = p->sweeps[i].nr;
+    if (s->dtype == SK_C64) {
+      SK_TRY((launch_one<float, 4>(s, p, i, c)));
+    } else if (nr == 4) {
+      SK_TRY((launch_one<double, 4>(s, p, i, c)));
+    } else {
+      SK_TRY((launch_one<double, 3>(s, p, i, c)));
+    }
   }
   return SK_OK;
 }
@@ -1193,15 +1198,19 @@ static int launch_sweeps(sk_state* s, const sk_program* p, int first, int count,
 static int lower_program(int width, int dtype, const sk_sweep* sweeps, int nsweeps, const sk_op* ops, int nops,
                          std::vector<DSweep>& dsw, std::vector<HostKOp>& kops) {
   if (dtype != SK_C64 && dtype != SK_C128) return set_error(SK_EVALUE, "bad dtype %d", dtype);
-  const int NR = dtype == SK_C64 ? kNR32 : kNR64;
-  const int maxT = dtype == SK_C64 ? kMaxTile32 : kMaxTile64;
+  const int NR0 = dtype == SK_C64 ? kNR32 : kNR64;
   const uint32_t esz = dtype == SK_C64 ? 8 : 16;
-  if (width < NR || width > 40) return set_error(SK_EVALUE, "fused program needs %d <= width <= 40", NR);
+  if (width < NR0 || width > 40) return set_error(SK_EVALUE, "fused program needs %d <= width <= 40", NR0);
   if (nsweeps < 0 || nops < 0) return set_error(SK_EVALUE, "negative counts");
   std::vector<int> op_seen(nops, 0);
   for (int si = 0; si < nsweeps; ++si) {
     const sk_sweep& sw = sweeps[si];
     DSweep d{};
+    const int NR = sw.nreg ? sw.nreg : NR0;
+    if (!(NR == 4 || (dtype == SK_C128 && NR == 3)))
+      return set_error(SK_EVALUE, "sweep %d: %d register bits not supported for this dtype", si, NR);
+    d.nr = NR;
+    const int maxT = dtype == SK_C64 ? kMaxTile32 : kMaxTile64;
     const int T = sw.ntile;
     if (T < NR || T > maxT || T > width) return set_error(SK_EVALUE, "sweep %d: bad tile bit count %d", si, T);
     int local_of[64];
@@ -1255,11 +1264,14 @@ static int lower_program(int width, int dtype, const sk_sweep* sweeps, int nswee
       for (int o = ob; o < oe; ++o) {
         if (op_seen[o]) return set_error(SK_EVALUE, "op %d used by two stages (sweep %d)", o, si);
         op_seen[o] = 1;
-        SK_TRY(lower_op(c, ops[o], o, width, kops, scale));
+        const size_t first = kops.size();
+      SK_TRY(lower_op(c, ops[o], o, width, kops, scale));
+      for (size_t k = first; k < kops.size(); ++k) kops[k].nr = NR;
       }
       if (s == sw.nstages - 1 && !(scale[0] == 1.0 && scale[1] == 0.0)) {  // deferred butterfly scalars
         HostKOp k;
         k.kind = K_PHASE;
+        k.nr = NR;
         k.emask = (1u << (1 << NR)) - 1;
         k.m[0] = k.m[2] = scale[0];
         k.m[1] = k.m[3] = scale[1];
@@ -1294,9 +1306,9 @@ int sk_program_create(int width, int dtype, int device, const sk_sweep* sweeps, 
   SK_TRY(ctx_get(device, &c));
   std::vector<unsigned char> buf;
   if (dtype == SK_C64)
-    pack_kops<float>(kops, buf, NR);
+    pack_kops<float>(kops, buf);
   else
-    pack_kops<double>(kops, buf, NR);
+    pack_kops<double>(kops, buf);
   sk_program* prog = new sk_program();
   prog->width = width;
   prog->dtype = dtype;
@@ -1308,8 +1320,8 @@ int sk_program_create(int width, int dtype, int device, const sk_sweep* sweeps, 
   prog->thr_off.assign(dsw.size(), 0);
   for (size_t i = 0; i < dsw.size(); ++i) {
     prog->thr_off[i] = thr.size();
-    append_thr(dsw[i], NR, dtype == SK_C64 ? 8 : 16, thr);
-    prog->qft_ok[i] = qsweep_from(dsw[i], kops, NR, &prog->qsweeps[i]);
+    append_thr(dsw[i], dtype == SK_C64 ? 8 : 16, thr);
+    prog->qft_ok[i] = qsweep_from(dsw[i], kops, &prog->qsweeps[i]);
   }
   if (!thr.empty()) {
     cudaError_t e = cudaMalloc(&prog->d_thr, thr.size() * sizeof(uint4));
@@ -1344,9 +1356,8 @@ int sk_program_lower(int width, int dtype, const sk_sweep* sweeps, int nsweeps, 
   std::vector<HostKOp> kops;
   std::vector<DSweep> dsw;
   SK_TRY(lower_program(width, dtype, sweeps, nsweeps, ops, nops, dsw, kops));
-  const int NR = dtype == SK_C64 ? kNR32 : kNR64;
   for (auto& k : kops)
-    if (k.kind == K_PHASE || k.kind == K_TPHASE) k.pat = pattern_of(NR, k.emask);
+    if (k.kind == K_PHASE || k.kind == K_TPHASE) k.pat = pattern_of(k.nr, k.emask);
   *count = (int)kops.size();
   if ((int)kops.size() > cap) return set_error(SK_EVALUE, "need room for %d kernel ops", (int)kops.size());
   for (size_t i = 0; i < kops.size(); ++i) {
@@ -1394,8 +1405,7 @@ int sk_program_run(sk_state* s, const sk_program* p, int first, int count) {
   if (first < 0 || first + count > ns) return set_error(SK_EVALUE, "sweep range [%d, %d) outside program", first, first + count);
   DevCtx* c;
   SK_TRY(ctx_get(s->device, &c));
-  if (s->dtype == SK_C64) return launch_sweeps<float, kNR32>(s, p, first, count, c);
-  return launch_sweeps<double, kNR64>(s, p, first, count, c);
+  return launch_sweeps(s, p, first, count, c);
 }
 
 }  // extern "C"

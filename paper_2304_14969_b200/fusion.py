@@ -40,10 +40,12 @@ MAX_STAGES = _lib.SK_MAX_STAGES
 
 # kernel geometry per dtype (csrc/sk_fused.cu): register bits, max tile bits,
 # low contiguous bits (256 B per warp access)
-GEOMETRY = {"c64": dict(nreg=4, tile=11, low=5, qft_tile=12, qft_low=4),
-            "c128": dict(nreg=3, tile=10, low=4, qft_tile=10, qft_low=4)}
+GEOMETRY = {"c64": dict(nreg=4, tile=11, low=5, qft_tile=12, qft_low=4, qft_nreg=4),
+            "c128": dict(nreg=3, tile=10, low=4, qft_tile=11, qft_low=3, qft_nreg=4)}
 # Measured on B200 (scripts/tune_qft.py): QFT-27 c64 1.10 ms at T=12/low=4
-# (k_qft); random 30x20 c64 384 ms at T=11/low=5 vs 467 ms at T=13/low=5 and
+# (k_qft); c128 QFT windows use 4 register bits (16 amplitudes per thread):
+# QFT-27 c128 2.44 ms in 3 sweeps at T=11/low=3 vs 2.98 ms in 4 sweeps with 3
+# register bits at T=10/low=4; random 30x20 c64 384 ms at T=11/low=5 vs 467 ms at T=13/low=5 and
 # c128 803 ms at T=10/low=4 vs 917 ms at T=12 (generic k_sweep: fewer, larger
 # tiles lose occupancy to its ~110 registers per thread).
 
@@ -347,7 +349,7 @@ def plan_qft(n: int, dtype: str = "c64", tile_bits: int | None = None, low_bits:
     top (each at most T - low bits, the bottom window up to T bits), each
     window split into register chunks of NR bits; one QFT op per chunk."""
     geo = GEOMETRY[dtype]
-    nreg = geo["nreg"]
+    nreg = geo["qft_nreg"]
     T = min(tile_bits or geo["qft_tile"], n)
     low = min(low_bits if low_bits is not None else geo["qft_low"], T)
     windows = []
@@ -423,6 +425,7 @@ def to_c(plan: Plan):
     for si, sp in enumerate(plan.sweeps):
         cs = sweeps[si]
         cs.ntile = len(sp.tile_bits)
+        cs.nreg = plan.nreg
         for i, b in enumerate(sp.tile_bits):
             cs.tile_bits[i] = b
         cs.nstages = len(sp.stages)

@@ -138,11 +138,11 @@ def sdrp54(budget_log2=31, depth=7, circuits=1):
              trace=[(t.p, t.ok, t.f_model, t.peak_amplitudes, round(t.wall_s, 3)) for t in trace])
 
 
-def hybrid(n=20):
+def hybrid(n=20, reps=3):
     from paper_2304_14969_b200.engine import EngineConfig, HybridState, OptFlags
     for dtype in ("c128", "c64"):
         ts = []
-        for rep in range(3):
+        for rep in range(reps):
             sim = HybridState(n, EngineConfig(mem_budget=1 << 30, dtype=dtype,
                                               optimizations=OptFlags(stabilizer_hybrid=False)))
             sim.apply_circuit(build_ghz(n))
@@ -153,7 +153,8 @@ def hybrid(n=20):
             sim.flush_all()
             torch.cuda.synchronize()
             ts.append(time.perf_counter() - t0)
-        emit(config=f"hybrid_qft{n}_ghz", dtype=dtype, wall_s=sorted(ts)[1], stats=dict(sim.stats))
+        emit(config=f"hybrid_qft{n}_ghz", dtype=dtype, wall_s=sorted(ts)[len(ts) // 2], stats=dict(sim.stats),
+             peak=sim.peak_amplitudes)
 
 
 if __name__ == "__main__":
@@ -170,5 +171,6 @@ if __name__ == "__main__":
         elif w.startswith("sdrp54"):  # sdrp54[:budget_log2[:circuits]]
             parts = w.split(":")
             sdrp54(int(parts[1]) if len(parts) > 1 else 31, 7, int(parts[2]) if len(parts) > 2 else 1)
-        elif w == "hybrid":
-            hybrid()
+        elif w.startswith("hybrid"):  # hybrid[:n]
+            parts = w.split(":")
+            hybrid(int(parts[1]) if len(parts) > 1 else 20, 3 if len(parts) == 1 or int(parts[1]) < 26 else 1)

@@ -100,7 +100,7 @@ def test_qft27_closed_forms(dtype):
     n = 27
     N = 1 << n
     prog = compile_circuit(build_qft(n), dtype=dtype)
-    assert prog.n_sweeps == (3 if dtype == "c64" else 4)
+    assert prog.n_sweeps == 3
     idx = np.random.default_rng(1).integers(0, N, 4096)
     from paper_2304_14969_b200.ket import permute_qubits
     # GHZ input (paper Fig. 1b)

@@ -60,7 +60,7 @@ def test_qft27_is_three_sweeps():
     assert len(plan.sweeps) == 3
     plan64 = fusion.plan_circuit(build_qft(27), dtype="c128")
     check_structure(plan64)
-    assert len(plan64.sweeps) == 4  # fp64 QFT windows use 10-bit tiles (scripts/tune_qft.py)
+    assert len(plan64.sweeps) == 3  # fp64 QFT windows: 4 register bits, 11-bit tiles (scripts/tune_qft.py)
 
 
 @pytest.mark.parametrize("seed", [1, 2, 3])
