@@ -72,8 +72,13 @@ struct alignas(16) KHdr {
   uint16_t emask;
   uint8_t lo, nbits;
   uint32_t flags;
-  uint32_t pad;
+  uint32_t opc;  // fast-path opcode for k_sweep's dispatch (OPC_*), 0 = interpret via apply_kop
 };
+
+// fast paths of the generic interpreter: the unpredicated dense 2x2 (every
+// U3 of a random circuit), the same behind a thread-side control, and the
+// controlled-X register swap; everything else goes through apply_kop
+enum KOpc : uint32_t { OPC_GENERIC = 0, OPC_MAT = 1, OPC_MATT = 5, OPC_SWAPT = 9 };
 
 template <typename R>
 struct alignas(16) KOp {
@@ -477,6 +482,38 @@ __device__ __forceinline__ void apply_kop(const KOp<R>* __restrict__ op, vec2_t<
   }
 }
 
+// unpredicated dense 2x2 on slot P: coefficients m and rotated mr as four
+// 16-byte loads, then 8 (fp32) paired ops per element pair
+template <typename R, int NR, int P>
+__device__ __forceinline__ void mat_full(vec2_t<R> (&a)[1 << NR], const KOp<R>* __restrict__ op) {
+  vec2_t<R> c[8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    c[2 * i] = mk<R>(op->m[2 * i], op->m[2 * i + 1]);
+    c[2 * i + 1] = mk<R>(op->mr[2 * i], op->mr[2 * i + 1]);
+  }
+#pragma unroll
+  for (int e = 0; e < (1 << NR); ++e) {
+    if ((e >> P) & 1) continue;
+    const int e1 = e | (1 << P);
+    const vec2_t<R> y0 = cmac2<R>(a[e], a[e1], c[0], c[1], c[2], c[3]);
+    const vec2_t<R> y1 = cmac2<R>(a[e], a[e1], c[4], c[5], c[6], c[7]);
+    a[e] = y0;
+    a[e1] = y1;
+  }
+}
+
+template <typename R, int NR, int P>
+__device__ __forceinline__ void swap_slot(vec2_t<R> (&a)[1 << NR]) {
+#pragma unroll
+  for (int e = 0; e < (1 << NR); ++e) {
+    if ((e >> P) & 1) continue;
+    const vec2_t<R> t = a[e];
+    a[e] = a[e | (1 << P)];
+    a[e | (1 << P)] = t;
+  }
+}
+
 // Generic fused sweep (random circuits, mixed gate streams): NS compile-time
 // stages with per-thread index parts from the host-built table `thr`
 // (uint4 per stage and thread: global bits lo/hi, swizzled shared offset),
@@ -518,7 +555,25 @@ __global__ void __launch_bounds__(512, 1) k_sweep(vec2_t<R>* __restrict__ amps, 
         a[e] = *reinterpret_cast<const V*>(smraw + so);
       }
     }
-    for (int o = st.op_begin; o < st.op_end; ++o) apply_kop<R, NR>(ops + o, a, gthr);
+    for (int o = st.op_begin; o < st.op_end; ++o) {
+      const KOp<R>* op = ops + o;
+      const uint32_t opc = op->h.opc;
+      switch (opc) {
+#define SK_FM(P)                                                                              \
+  case OPC_MAT + P:                                                                           \
+    if (P < NR) mat_full<R, NR, (P < NR ? P : 0)>(a, op);                                     \
+    break;                                                                                    \
+  case OPC_MATT + P:                                                                          \
+    if (P < NR && (gthr & op->tmask) == op->tval) mat_full<R, NR, (P < NR ? P : 0)>(a, op); \
+    break;                                                                                    \
+  case OPC_SWAPT + P:                                                                         \
+    if (P < NR && (gthr & op->tmask) == op->tval) swap_slot<R, NR, (P < NR ? P : 0)>(a);    \
+    break;
+        SK_FM(0) SK_FM(1) SK_FM(2) SK_FM(3)
+#undef SK_FM
+        default: apply_kop<R, NR>(op, a, gthr); break;
+      }
+    }
     if (s == NS - 1) {
       char* p = reinterpret_cast<char*>(amps + gthr);
 #pragma unroll
@@ -1026,6 +1081,15 @@ static int lower_op(const StageCtx& c, const sk_op& op, int o, int width, std::v
   return set_error(SK_EVALUE, "op %d: unknown kind %d", o, op.kind);
 }
 
+static uint32_t opcode_of(const HostKOp& k) {
+  if (k.slot < 0 || k.slot >= k.nr || (k.flags & ~(uint32_t)F_TPRED)) return OPC_GENERIC;
+  if (k.emask != slot_mask(k.nr, k.slot, 0)) return OPC_GENERIC;
+  const bool tp = (k.flags & F_TPRED) != 0;
+  if (k.kind == K_MAT) return (tp ? OPC_MATT : OPC_MAT) + k.slot;
+  if (k.kind == K_MATR && k.m[0] == 0 && k.m[2] == 1 && k.m[4] == 1 && k.m[6] == 0) return OPC_SWAPT + k.slot;
+  return OPC_GENERIC;
+}
+
 template <typename R>
 static void pack_kops(std::vector<HostKOp>& h, std::vector<unsigned char>& buf) {
   buf.assign(sizeof(KOp<R>) * h.size(), 0);
@@ -1040,6 +1104,7 @@ static void pack_kops(std::vector<HostKOp>& h, std::vector<unsigned char>& buf) 
     x.h.lo = (uint8_t)h[i].lo;
     x.h.nbits = (uint8_t)h[i].nbits;
     x.h.flags = h[i].flags;
+    x.h.opc = opcode_of(h[i]);
     x.tmask = h[i].tmask;
     x.tval = h[i].tval;
     x.qmask = h[i].qmask;
