@@ -487,10 +487,12 @@ __device__ __forceinline__ void apply_kop(const KOp<R>* __restrict__ op, vec2_t<
 template <typename R, int NR, int P>
 __device__ __forceinline__ void mat_full(vec2_t<R> (&a)[1 << NR], const KOp<R>* __restrict__ op) {
   vec2_t<R> c[8];
+  const vec2_t<R>* mv = reinterpret_cast<const vec2_t<R>*>(op->m);
+  const vec2_t<R>* mrv = reinterpret_cast<const vec2_t<R>*>(op->mr);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    c[2 * i] = mk<R>(op->m[2 * i], op->m[2 * i + 1]);
-    c[2 * i + 1] = mk<R>(op->mr[2 * i], op->mr[2 * i + 1]);
+    c[2 * i] = __ldg(mv + i);
+    c[2 * i + 1] = __ldg(mrv + i);
   }
 #pragma unroll
   for (int e = 0; e < (1 << NR); ++e) {
@@ -555,24 +557,31 @@ __global__ void __launch_bounds__(512, 1) k_sweep(vec2_t<R>* __restrict__ amps, 
         a[e] = *reinterpret_cast<const V*>(smraw + so);
       }
     }
-    for (int o = st.op_begin; o < st.op_end; ++o) {
-      const KOp<R>* op = ops + o;
-      const uint32_t opc = op->h.opc;
-      switch (opc) {
-#define SK_FM(P)                                                                              \
-  case OPC_MAT + P:                                                                           \
-    if (P < NR) mat_full<R, NR, (P < NR ? P : 0)>(a, op);                                     \
-    break;                                                                                    \
-  case OPC_MATT + P:                                                                          \
-    if (P < NR && (gthr & op->tmask) == op->tval) mat_full<R, NR, (P < NR ? P : 0)>(a, op); \
-    break;                                                                                    \
-  case OPC_SWAPT + P:                                                                         \
-    if (P < NR && (gthr & op->tmask) == op->tval) swap_slot<R, NR, (P < NR ? P : 0)>(a);    \
+    // runs of fast-path ops and of interpreted ops in separate loops, so the
+    // fast loop keeps a[] in fixed registers (one loop with both made ptxas
+    // shuffle all 32 amplitude registers on every iteration)
+    for (int o = st.op_begin; o < st.op_end;) {
+      for (; o < st.op_end; ++o) {
+        const KOp<R>* op = ops + o;
+        const uint32_t opc = op->h.opc;
+        if (opc == OPC_GENERIC) break;
+        switch (opc) {
+#define SK_FM(P)                                                                                \
+  case OPC_MAT + P:                                                                             \
+    if (P < NR) mat_full<R, NR, (P < NR ? P : 0)>(a, op);                                       \
+    break;                                                                                      \
+  case OPC_MATT + P:                                                                            \
+    if (P < NR && (gthr & op->tmask) == op->tval) mat_full<R, NR, (P < NR ? P : 0)>(a, op);   \
+    break;                                                                                      \
+  case OPC_SWAPT + P:                                                                           \
+    if (P < NR && (gthr & op->tmask) == op->tval) swap_slot<R, NR, (P < NR ? P : 0)>(a);      \
     break;
-        SK_FM(0) SK_FM(1) SK_FM(2) SK_FM(3)
+          SK_FM(0) SK_FM(1) SK_FM(2) SK_FM(3)
 #undef SK_FM
-        default: apply_kop<R, NR>(op, a, gthr); break;
+          default: break;
+        }
       }
+      for (; o < st.op_end && ops[o].h.opc == OPC_GENERIC; ++o) apply_kop<R, NR>(ops + o, a, gthr);
     }
     if (s == NS - 1) {
       char* p = reinterpret_cast<char*>(amps + gthr);
