@@ -161,7 +161,7 @@ int sk_sample(const sk_state* s, const double* uniforms, int64_t k, int64_t* out
  * and applies its stages' ops on register-resident amplitudes.  See
  * DESIGN.md "Fused sweep kernel". */
 #define SK_MAX_TILE_BITS 16
-#define SK_MAX_REG_BITS 4
+#define SK_MAX_REG_BITS 5
 #define SK_MAX_STAGES 8
 
 #define SK_OP_MAT 0   /* 2x2 matrix on register slot `slot`, predicated      */
@@ -187,7 +187,7 @@ typedef struct {
   int32_t reg_bits[SK_MAX_STAGES][SK_MAX_REG_BITS]; /* global qubits held in registers */
   int32_t op_begin[SK_MAX_STAGES + 1];        /* stage s runs ops[op_begin[s] .. op_begin[s+1]) */
   int32_t nreg;                               /* register bits per stage: 0 = sk_program_reg_bits default;
-                                                 c64: 4, c128: 3 or 4 (QFT windows use 4) */
+                                                 c64: 4 (5 for QFT-window sweeps), c128: 3 or 4 */
 } sk_sweep;
 
 /* Validate and upload a program for an n-qubit state of `dtype`.  Each

@@ -14,7 +14,7 @@ from .errors import DeviceError, MemoryBudgetError
 SK_OK, SK_EINDEX, SK_EVALUE, SK_ENOMEM, SK_ECUDA = 0, 1, 2, 3, 4
 SK_C64, SK_C128 = 0, 1
 SK_OP_MAT, SK_OP_DIAG, SK_OP_RAMP, SK_OP_QFT = 0, 1, 2, 3
-SK_MAX_TILE_BITS, SK_MAX_REG_BITS, SK_MAX_STAGES = 16, 4, 8
+SK_MAX_TILE_BITS, SK_MAX_REG_BITS, SK_MAX_STAGES = 16, 5, 8
 
 DTYPES = {"c64": SK_C64, "complex64": SK_C64, "c128": SK_C128, "complex128": SK_C128}
 

@@ -648,17 +648,27 @@ __device__ __forceinline__ uint64_t deposit_q(uint64_t x, const Run* r, int n) {
   return o;
 }
 
+// cos(pi K / 16) for K = 0..15 (sin(pi K / 16) = cos16(8 - K) for K <= 8)
+__host__ __device__ constexpr double cos16(int K) {
+  return K == 0 ? 1.0 : K == 1 ? 0.98078528040323044 : K == 2 ? 0.92387953251128674 : K == 3 ? 0.83146961230254524
+       : K == 4 ? 0.70710678118654752 : K == 5 ? 0.55557023301960218 : K == 6 ? 0.38268343236508978
+       : K == 7 ? 0.19509032201612826 : K == 8 ? 0.0 : -cos16(16 - K);
+}
+__host__ __device__ constexpr double sin16(int K) { return K <= 8 ? cos16(8 - K) : cos16(K - 8); }
+
 template <typename R, int K>
-__device__ __forceinline__ vec2_t<R> pk_pi8(vec2_t<R> x) {  // x * exp(i pi K / 8), K compile-time
+__device__ __forceinline__ vec2_t<R> pk_pi16(vec2_t<R> x) {  // x * exp(i pi K / 16), 0 <= K < 16 compile-time
   if constexpr (K == 0) return x;
-  else if constexpr (K == 4) return mk<R>(-x.y, x.x);
-  else {
-    constexpr double c = K == 1 ? 0.92387953251128674 : K == 2 ? 0.70710678118654752 : K == 3 ? 0.38268343236508978
-                       : K == 5 ? -0.38268343236508978 : K == 6 ? -0.70710678118654752 : -0.92387953251128674;
-    constexpr double s = K == 1 ? 0.38268343236508978 : K == 2 ? 0.70710678118654752 : K == 3 ? 0.92387953251128674
-                       : K == 5 ? 0.92387953251128674 : K == 6 ? 0.70710678118654752 : 0.38268343236508978;
-    return PK<R>::mul(x, mk<R>((R)c, (R)s));
-  }
+  else if constexpr (K == 8) return mk<R>(-x.y, x.x);
+  else return PK<R>::mul(x, mk<R>((R)cos16(K), (R)sin16(K)));
+}
+
+template <int NR, int L, int TOP, int P, int E>
+__host__ __device__ constexpr int qft_k16() {  // internal twiddle of pair base E at layer slot P, units of pi/16
+  int k = 0;
+  for (int p = TOP - L + 1; p < P; ++p)
+    if ((E >> p) & 1) k += 1 << (4 - (P - p));
+  return k;
 }
 
 template <typename R, int NR, int L, int TOP, int P, int E>
@@ -669,7 +679,7 @@ __device__ __forceinline__ void pk_pair(vec2_t<R> (&a)[1 << NR]) {
       const vec2_t<R> s = PK<R>::add(a[E], a[E1]);
       const vec2_t<R> d = PK<R>::sub(a[E], a[E1]);
       a[E] = s;
-      a[E1] = pk_pi8<R, qft_k8<NR, L, TOP, P, E>()>(d);
+      a[E1] = pk_pi16<R, qft_k16<NR, L, TOP, P, E>()>(d);
     }
     pk_pair<R, NR, L, TOP, P, E + 1>(a);
   }
@@ -738,12 +748,13 @@ __device__ __forceinline__ void pk_chunk(const QStage& st, vec2_t<R> (&a)[1 << N
   }
 }
 
-// fp64 gets the larger register budget (its tiles are 2^(T-3) <= 256 threads)
-template <typename R>
-constexpr int qft_max_threads() { return sizeof(R) == 4 ? 512 : 256; }
+// 16 fp32 amplitudes per thread fit 64 registers (512 threads x 2 CTAs);
+// 32 fp32 or 16 fp64 amplitudes get 128 (tiles of <= 256 threads)
+template <typename R, int NR>
+constexpr int qft_max_threads() { return (sizeof(R) == 4 && NR <= 4) ? 512 : 256; }
 
 template <typename R, int NR, int NS>
-__global__ void __launch_bounds__(qft_max_threads<R>(), 2) k_qft(vec2_t<R>* __restrict__ amps, const __grid_constant__ QSweep sw) {
+__global__ void __launch_bounds__(qft_max_threads<R, NR>(), 2) k_qft(vec2_t<R>* __restrict__ amps, const __grid_constant__ QSweep sw) {
   using V = vec2_t<R>;
   extern __shared__ __align__(16) unsigned char smraw[];
   constexpr int NE = 1 << NR;
@@ -780,10 +791,11 @@ __global__ void __launch_bounds__(qft_max_threads<R>(), 2) k_qft(vec2_t<R>* __re
     switch (st.code) {
 #define SK_QC(L, TOP) \
   case L * 8 + TOP: pk_chunk<R, NR, L, TOP>(st, a, gthr); break;
-      SK_QC(1, 0) SK_QC(1, 1) SK_QC(1, 2) SK_QC(1, 3)
-      SK_QC(2, 1) SK_QC(2, 2) SK_QC(2, 3)
-      SK_QC(3, 2) SK_QC(3, 3)
-      SK_QC(4, 3)
+      SK_QC(1, 0) SK_QC(1, 1) SK_QC(1, 2) SK_QC(1, 3) SK_QC(1, 4)
+      SK_QC(2, 1) SK_QC(2, 2) SK_QC(2, 3) SK_QC(2, 4)
+      SK_QC(3, 2) SK_QC(3, 3) SK_QC(3, 4)
+      SK_QC(4, 3) SK_QC(4, 4)
+      SK_QC(5, 4)
 #undef SK_QC
       default: break;
     }
@@ -1216,9 +1228,11 @@ static int launch_one(sk_state* s, const sk_program* p, int i, DevCtx* c) {
   static bool attr_set[64] = {false};
   if (!attr_set[s->device]) {
 #define SK_ATTR(K) SK_CUDA(cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024))
-    SK_ATTR((k_sweep<R, NR, 1>)); SK_ATTR((k_sweep<R, NR, 2>)); SK_ATTR((k_sweep<R, NR, 3>));
-    SK_ATTR((k_sweep<R, NR, 4>)); SK_ATTR((k_sweep<R, NR, 5>)); SK_ATTR((k_sweep<R, NR, 6>));
-    SK_ATTR((k_sweep<R, NR, 7>)); SK_ATTR((k_sweep<R, NR, 8>));
+    if constexpr (NR <= 4) {
+      SK_ATTR((k_sweep<R, NR, 1>)); SK_ATTR((k_sweep<R, NR, 2>)); SK_ATTR((k_sweep<R, NR, 3>));
+      SK_ATTR((k_sweep<R, NR, 4>)); SK_ATTR((k_sweep<R, NR, 5>)); SK_ATTR((k_sweep<R, NR, 6>));
+      SK_ATTR((k_sweep<R, NR, 7>)); SK_ATTR((k_sweep<R, NR, 8>));
+    }
     SK_ATTR((k_qft<R, NR, 1>)); SK_ATTR((k_qft<R, NR, 2>)); SK_ATTR((k_qft<R, NR, 3>));
     SK_ATTR((k_qft<R, NR, 4>)); SK_ATTR((k_qft<R, NR, 5>)); SK_ATTR((k_qft<R, NR, 6>));
 #undef SK_ATTR
@@ -1231,7 +1245,7 @@ static int launch_one(sk_state* s, const sk_program* p, int i, DevCtx* c) {
   const size_t smem = ((size_t)1 << T) * sizeof(vec2_t<R>);
   if (tiles > 0x7fffffffull) return set_error(SK_EVALUE, "too many tiles (%d bits outside the tile)", s->width - T);
   vec2_t<R>* d_amps = (vec2_t<R>*)s->d;
-  if (p->qft_ok[i] && threads <= (unsigned)qft_max_threads<R>() && use_qft_kernel()) {
+  if (p->qft_ok[i] && threads <= (unsigned)qft_max_threads<R, NR>() && (NR > 4 || use_qft_kernel())) {
     const QSweep& q = p->qsweeps[i];
     switch (q.nstages) {
 #define SK_QS(NS_) \
@@ -1240,6 +1254,8 @@ static int launch_one(sk_state* s, const sk_program* p, int i, DevCtx* c) {
 #undef SK_QS
       default: return set_error(SK_EVALUE, "sweep %d: %d stages", i, q.nstages);
     }
+  } else if constexpr (NR > 4) {
+    return set_error(SK_EVALUE, "sweep %d: %d register bits need the QFT-window kernel", i, NR);
   } else {
     const KOp<R>* ops = (const KOp<R>*)p->d_ops;
     const uint4* thr = (const uint4*)p->d_thr + p->thr_off[i];
@@ -1258,7 +1274,9 @@ static int launch_one(sk_state* s, const sk_program* p, int i, DevCtx* c) {
 static int launch_sweeps(sk_state* s, const sk_program* p, int first, int count, DevCtx* c) {
   for (int i = first; i < first + count; ++i) {
     const int nr = p->sweeps[i].nr;
-    if (s->dtype == SK_C64) {
+    if (s->dtype == SK_C64 && nr == 5) {
+      SK_TRY((launch_one<float, 5>(s, p, i, c)));
+    } else if (s->dtype == SK_C64) {
       SK_TRY((launch_one<float, 4>(s, p, i, c)));
     } else if (nr == 4) {
       SK_TRY((launch_one<double, 4>(s, p, i, c)));
@@ -1281,8 +1299,13 @@ static int lower_program(int width, int dtype, const sk_sweep* sweeps, int nswee
     const sk_sweep& sw = sweeps[si];
     DSweep d{};
     const int NR = sw.nreg ? sw.nreg : NR0;
-    if (!(NR == 4 || (dtype == SK_C128 && NR == 3)))
+    if (!(NR == 4 || (dtype == SK_C128 && NR == 3) || (dtype == SK_C64 && NR == 5)))
       return set_error(SK_EVALUE, "sweep %d: %d register bits not supported for this dtype", si, NR);
+    if (NR == 5)  // 32-element register sets exist only in the QFT-window kernel
+      for (int s = 0; s < sw.nstages; ++s)
+        for (int o = sw.op_begin[s]; o < sw.op_begin[s + 1]; ++o)
+          if (o >= 0 && o < nops && ops[o].kind != SK_OP_QFT)
+            return set_error(SK_EVALUE, "sweep %d: 5 register bits are only supported for QFT-window ops", si);
     d.nr = NR;
     const int maxT = dtype == SK_C64 ? kMaxTile32 : kMaxTile64;
     const int T = sw.ntile;
@@ -1346,7 +1369,7 @@ static int lower_program(int width, int dtype, const sk_sweep* sweeps, int nswee
         HostKOp k;
         k.kind = K_PHASE;
         k.nr = NR;
-        k.emask = (1u << (1 << NR)) - 1;
+        k.emask = (uint32_t)((1ull << (1 << NR)) - 1);
         k.m[0] = k.m[2] = scale[0];
         k.m[1] = k.m[3] = scale[1];
         kops.push_back(k);

@@ -40,7 +40,7 @@ MAX_STAGES = _lib.SK_MAX_STAGES
 
 # kernel geometry per dtype (csrc/sk_fused.cu): register bits, max tile bits,
 # low contiguous bits (256 B per warp access)
-GEOMETRY = {"c64": dict(nreg=4, tile=11, low=5, qft_tile=12, qft_low=4, qft_nreg=4),
+GEOMETRY = {"c64": dict(nreg=4, tile=11, low=5, qft_tile=13, qft_low=4, qft_nreg=5),
             "c128": dict(nreg=3, tile=10, low=4, qft_tile=11, qft_low=3, qft_nreg=4)}
 # Measured on B200 (scripts/tune_qft.py): QFT-27 c64 1.10 ms at T=12/low=4
 # (k_qft); c128 QFT windows use 4 register bits (16 amplitudes per thread):
@@ -344,12 +344,14 @@ def match_qft(ops: list[Op], n: int) -> bool:
 
 
 def plan_qft(n: int, dtype: str = "c64", tile_bits: int | None = None, low_bits: int | None = None,
-             phys=None, n_gates: int = 0) -> Plan:
+             phys=None, n_gates: int = 0, nreg: int | None = None) -> Plan:
     """Sweeps for the QFT body in FFT form: windows of target bits from the
     top (each at most T - low bits, the bottom window up to T bits), each
     window split into register chunks of NR bits; one QFT op per chunk."""
     geo = GEOMETRY[dtype]
-    nreg = geo["qft_nreg"]
+    nreg = nreg or geo["qft_nreg"]
+    if nreg > 4 and n < 2 * nreg:  # small registers: 4-bit chunks (the 5-bit kernel wants >= 2 chunks of room)
+        nreg = 4
     T = min(tile_bits or geo["qft_tile"], n)
     low = min(low_bits if low_bits is not None else geo["qft_low"], T)
     windows = []
@@ -405,14 +407,14 @@ def plan_qft(n: int, dtype: str = "c64", tile_bits: int | None = None, low_bits:
 
 
 def plan_circuit(circuit: Circuit, dtype: str = "c64", tile_bits: int | None = None,
-                 low_bits: int | None = None, fuse: bool = True, qft: bool = True) -> Plan:
+                 low_bits: int | None = None, fuse: bool = True, qft: bool = True, qft_nreg: int | None = None) -> Plan:
     ops, phys = lower(circuit)
     if fuse:
         ops = fuse_diagonal_runs(ops)
     geo = GEOMETRY[dtype]
     if qft and fuse and circuit.width >= geo["nreg"] + 1 and match_qft(ops, circuit.width):
         try:
-            return plan_qft(circuit.width, dtype, tile_bits, low_bits, phys, len(circuit.gates))
+            return plan_qft(circuit.width, dtype, tile_bits, low_bits, phys, len(circuit.gates), qft_nreg)
         except ValueError:
             pass  # geometry the QFT form cannot pad: fall back to generic sweeps
     return plan_ops(ops, circuit.width, dtype, tile_bits, low_bits, phys, len(circuit.gates))

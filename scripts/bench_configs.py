@@ -138,6 +138,27 @@ def sdrp54(budget_log2=31, depth=7, circuits=1):
              trace=[(t.p, t.ok, t.f_model, t.peak_amplitudes, round(t.wall_s, 3)) for t in trace])
 
 
+def sdrp_depths(budget_log2=30, circuits=10, depths=(7, 8, 9, 10)):
+    """Paper-style ensemble: per depth, min-SDRP search for
+    `circuits` random 54-qubit circuits (validate.py:280-300 semantics) at a
+    device budget; mean / median F_model and time per circuit."""
+    import statistics
+    from paper_2304_14969_b200.circuit import derive_seed
+    from paper_2304_14969_b200.sdrp import min_sdrp_search
+    for d in depths:
+        fs, ps, ts, peaks = [], [], [], []
+        for i in range(circuits):
+            t0 = time.perf_counter()
+            r = min_sdrp_search(54, d, derive_seed(0, i), 1 << budget_log2, dtype="c64")
+            ts.append(time.perf_counter() - t0)
+            fs.append(r.f_model if r.feasible else 0.0)
+            ps.append(r.p_min if r.feasible else None)
+            peaks.append(r.peak_amplitudes)
+        emit(config="sdrp54_depths", depth=d, circuits=circuits, budget=1 << budget_log2,
+             f_model_mean=statistics.mean(fs), f_model_median=statistics.median(fs), f_model_max=max(fs),
+             p_min=ps, peak_max=max(peaks), s_per_circuit=statistics.mean(ts))
+
+
 def hybrid(n=20, reps=3):
     from paper_2304_14969_b200.engine import EngineConfig, HybridState, OptFlags
     for dtype in ("c128", "c64"):
@@ -171,6 +192,9 @@ if __name__ == "__main__":
         elif w.startswith("sdrp54"):  # sdrp54[:budget_log2[:circuits]]
             parts = w.split(":")
             sdrp54(int(parts[1]) if len(parts) > 1 else 31, 7, int(parts[2]) if len(parts) > 2 else 1)
+        elif w.startswith("sdrpdepths"):  # sdrpdepths[:budget_log2[:circuits]]
+            parts = w.split(":")
+            sdrp_depths(int(parts[1]) if len(parts) > 1 else 30, int(parts[2]) if len(parts) > 2 else 10)
         elif w.startswith("hybrid"):  # hybrid[:n]
             parts = w.split(":")
             hybrid(int(parts[1]) if len(parts) > 1 else 20, 3 if len(parts) == 1 or int(parts[1]) < 26 else 1)

@@ -1,5 +1,6 @@
 """Time QFT-n fused programs across tile geometries (per-sweep CUDA-event
 timings, warm, state >> L2).  Usage: python scripts/tune_qft.py [n] [dtype]"""
+import os
 import sys
 from pathlib import Path
 
@@ -21,11 +22,13 @@ _lib.call("sk_set_stream", 0, stream.cuda_stream)
 st = DenseKet(n, dtype=dtype)
 c = build_qft(n) if circ == "qft" else build_random_circuit(n, 20, 1)
 esz = 8 if dtype == "c64" else 16
-tiles = [11, 12, 13] if dtype == "c64" else [10, 11, 12]
+tiles = [int(t) for t in os.environ["TILES"].split(",")] if "TILES" in os.environ else (
+    [11, 12, 13] if dtype == "c64" else [10, 11, 12])
 for T in tiles:
     for low in (3, 4, 5):
         try:
-            prog = compile_circuit(c, dtype=dtype, tile_bits=T, low_bits=low)
+            kw = {"qft_nreg": int(os.environ["QFT_NREG"])} if "QFT_NREG" in os.environ else {}
+            prog = compile_circuit(c, dtype=dtype, tile_bits=T, low_bits=low, **kw)
         except Exception as exc:  # noqa: BLE001
             print(T, low, "plan failed", exc)
             continue

@@ -39,4 +39,4 @@ def test_no_device_is_reported_not_faked():
 
 def test_struct_layouts_match_header():
     assert ctypes.sizeof(_lib.SkOp) == 4 * 4 + 8 * 2 + 8 * 8
-    assert ctypes.sizeof(_lib.SkSweep) == 4 * (1 + 16 + 1 + 8 * 4 + 9 + 1)
+    assert ctypes.sizeof(_lib.SkSweep) == 4 * (1 + 16 + 1 + 8 * 5 + 9 + 1)

@@ -101,4 +101,5 @@ def test_to_c_roundtrip():
     plan = fusion.plan_circuit(build_qft(16), dtype="c64")
     sweeps, ops, nops = fusion.to_c(plan)
     assert nops == sum(len(st.ops) for sp in plan.sweeps for st in sp.stages)
-    assert sweeps[0].ntile == 12 and sweeps[-1].op_begin[sweeps[-1].nstages] == nops
+    assert sweeps[0].ntile == fusion.GEOMETRY["c64"]["qft_tile"] and sweeps[-1].op_begin[sweeps[-1].nstages] == nops
+    assert all(sweeps[i].nreg == plan.nreg for i in range(len(plan.sweeps)))

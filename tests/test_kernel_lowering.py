@@ -75,11 +75,11 @@ def qft_chunk(amps, g, gthr, regs, e_of, slot, lo, nbits, flags, tmask, tval, qm
         i0 = np.nonzero(((g >> np.uint64(q)) & np.uint64(1)) == 0)[0]
         i1 = i0 | (1 << q)
         a0, a1 = amps[i0].copy(), amps[i1].copy()
-        k8 = np.zeros(i0.size, dtype=np.int64)
+        k16 = np.zeros(i0.size, dtype=np.int64)
         for p in range(top - L + 1, P):
-            k8 += ((e_of[i0] >> p) & 1) << (3 - (P - p))
+            k16 += ((e_of[i0] >> p) & 1) << (4 - (P - p))
         amps[i0] = a0 + a1
-        amps[i1] = (a0 - a1) * np.exp(1j * np.pi * k8 / 8)
+        amps[i1] = (a0 - a1) * np.exp(1j * np.pi * k16 / 16)
     if flags & F_END:
         t = np.zeros_like(gthr)
         for p in layer_slots:
