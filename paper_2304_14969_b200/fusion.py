@@ -40,12 +40,15 @@ MAX_STAGES = _lib.SK_MAX_STAGES
 
 # kernel geometry per dtype (csrc/sk_fused.cu): register bits, max tile bits,
 # low contiguous bits (256 B per warp access)
-GEOMETRY = {"c64": dict(nreg=4, tile=11, low=5, qft_tile=13, qft_low=4, qft_nreg=5),
+GEOMETRY = {"c64": dict(nreg=4, tile=11, low=5, qft_tile=12, qft_low=4, qft_nreg=4),
             "c128": dict(nreg=3, tile=10, low=4, qft_tile=11, qft_low=3, qft_nreg=4)}
 # Measured on B200 (scripts/tune_qft.py): QFT-27 c64 1.10 ms at T=12/low=4
 # (k_qft); c128 QFT windows use 4 register bits (16 amplitudes per thread):
 # QFT-27 c128 2.44 ms in 3 sweeps at T=11/low=3 vs 2.98 ms in 4 sweeps with 3
-# register bits at T=10/low=4; random 30x20 c64 384 ms at T=11/low=5 vs 467 ms at T=13/low=5 and
+# register bits at T=10/low=4; c64 5-bit QFT chunks (qft_nreg=5, 32
+# amplitudes per thread, 2/2/3 stages at T=13) measured 1.18 ms vs 1.09 ms
+# for 4-bit chunks at T=12 (half the occupancy costs more than the saved
+# exchange); random 30x20 c64 384 ms at T=11/low=5 vs 467 ms at T=13/low=5 and
 # c128 803 ms at T=10/low=4 vs 917 ms at T=12 (generic k_sweep: fewer, larger
 # tiles lose occupancy to its ~110 registers per thread).
 

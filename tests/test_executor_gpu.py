@@ -25,6 +25,18 @@ pytestmark = pytest.mark.gpu
 TOL = {"c128": 1e-12, "c64": 1e-5}
 
 
+@pytest.mark.parametrize("n", [10, 13, 16])
+def test_qft_five_register_bits_vs_oracle(rng, n):
+    x = random_state(n, rng)
+    prog = compile_circuit(build_qft(n), dtype="c64", tile_bits=min(n, 13), low_bits=4, qft_nreg=5)
+    assert prog.plan.nreg == 5
+    s = DenseKet(n, x, dtype="c64")
+    prog.run(s)
+    from paper_2304_14969_b200.ket import permute_qubits
+    got = permute_qubits(s, prog.plan.order).amps
+    assert np.max(np.abs(got - O.dft_oracle(x))) < 1e-5
+
+
 @pytest.mark.parametrize("dtype", ["c128", "c64"])
 def test_qft_small_vs_oracle_and_dft(rng, dtype):
     for n in range(2, 15):
@@ -94,12 +106,14 @@ def test_mixed_controls_swaps_and_measurement(rng):
         dense_reference(cm, initial=DenseKet(n, x))
 
 
-@pytest.mark.parametrize("dtype", ["c64", "c128"])
-def test_qft27_closed_forms(dtype):
-    """Config D2 (27 qubits, 1xB200) checked with size-independent closed forms."""
+@pytest.mark.parametrize("dtype,qft_nreg", [("c64", None), ("c128", None), ("c64", 5)])
+def test_qft27_closed_forms(dtype, qft_nreg):
+    """Config D2 (27 qubits, 1xB200) checked with size-independent closed forms
+    (qft_nreg=5: the 32-amplitudes-per-thread QFT-window kernel)."""
     n = 27
     N = 1 << n
-    prog = compile_circuit(build_qft(n), dtype=dtype)
+    kw = dict(tile_bits=13, low_bits=4, qft_nreg=5) if qft_nreg else {}
+    prog = compile_circuit(build_qft(n), dtype=dtype, **kw)
     assert prog.n_sweeps == 3
     idx = np.random.default_rng(1).integers(0, N, 4096)
     from paper_2304_14969_b200.ket import permute_qubits

@@ -103,3 +103,11 @@ def test_to_c_roundtrip():
     assert nops == sum(len(st.ops) for sp in plan.sweeps for st in sp.stages)
     assert sweeps[0].ntile == fusion.GEOMETRY["c64"]["qft_tile"] and sweeps[-1].op_begin[sweeps[-1].nstages] == nops
     assert all(sweeps[i].nreg == plan.nreg for i in range(len(plan.sweeps)))
+
+
+def test_qft_five_register_bit_chunks():
+    """c64 QFT windows can use 5 register bits (32 amplitudes per thread):
+    windows of 9 bits split [4, 5], QFT-27 = 3 sweeps of 2/2/3 stages."""
+    plan = fusion.plan_circuit(build_qft(27), dtype="c64", tile_bits=13, low_bits=4, qft_nreg=5)
+    assert plan.nreg == 5 and [len(sp.stages) for sp in plan.sweeps] == [2, 2, 3]
+    assert [op.nbits for st in plan.sweeps[0].stages for op in st.ops] == [4, 5]
