@@ -59,6 +59,7 @@ struct DSweep {
   int ntile;
   int nstages;
   int nr;        // register bits per stage (4 for c64; 3 or 4 for c128)
+  int lean;      // every kernel op has a fast-path opcode (k_sweep<..., LEAN>)
   int qft_only;  // every kernel op is a K_QFTS chunk: use the specialised kernel
   int nb;
   Run brun[kMaxRuns];  // tile index (blockIdx) bits -> non-tile global bits
@@ -78,7 +79,16 @@ struct alignas(16) KHdr {
 // fast paths of the generic interpreter: the unpredicated dense 2x2 (every
 // U3 of a random circuit), the same behind a thread-side control, and the
 // controlled-X register swap; everything else goes through apply_kop
-enum KOpc : uint32_t { OPC_GENERIC = 0, OPC_MAT = 1, OPC_MATT = 5, OPC_SWAPT = 9 };
+enum KOpc : uint32_t {
+  OPC_GENERIC = 0,
+  OPC_MAT = 1,     // + P: dense 2x2 on slot P, unpredicated
+  OPC_MATT = 5,    // + P: same behind a thread-side predicate
+  OPC_SWAPT = 9,   // + P: X on slot P (register swap), optional thread predicate
+  OPC_MATQ = 16,   // + 2 (4P + Q) + V: dense 2x2 on slot P where register slot Q == V
+  OPC_SWAPQ = 48,  // + 2 (4P + Q) + V: X on slot P where register slot Q == V
+  OPC_PHASE = 80,  // K_PHASE with a specialised element pattern
+  OPC_END = 81
+};
 
 template <typename R>
 struct alignas(16) KOp {
@@ -516,11 +526,91 @@ __device__ __forceinline__ void swap_slot(vec2_t<R> (&a)[1 << NR]) {
   }
 }
 
+// dense 2x2 on slot P restricted to the pairs whose register slot Q == V
+template <typename R, int NR, int P, int Q, int V>
+__device__ __forceinline__ void mat_q(vec2_t<R> (&a)[1 << NR], const KOp<R>* __restrict__ op) {
+  if constexpr (P < NR && Q < NR && P != Q) {
+    vec2_t<R> c[8];
+    const vec2_t<R>* mv = reinterpret_cast<const vec2_t<R>*>(op->m);
+    const vec2_t<R>* mrv = reinterpret_cast<const vec2_t<R>*>(op->mr);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      c[2 * i] = __ldg(mv + i);
+      c[2 * i + 1] = __ldg(mrv + i);
+    }
+#pragma unroll
+    for (int e = 0; e < (1 << NR); ++e) {
+      if (((e >> P) & 1) || ((e >> Q) & 1) != V) continue;
+      const int e1 = e | (1 << P);
+      const vec2_t<R> y0 = cmac2<R>(a[e], a[e1], c[0], c[1], c[2], c[3]);
+      const vec2_t<R> y1 = cmac2<R>(a[e], a[e1], c[4], c[5], c[6], c[7]);
+      a[e] = y0;
+      a[e1] = y1;
+    }
+  }
+}
+
+template <typename R, int NR, int P, int Q, int V>
+__device__ __forceinline__ void swap_q(vec2_t<R> (&a)[1 << NR]) {
+  if constexpr (P < NR && Q < NR && P != Q) {
+#pragma unroll
+    for (int e = 0; e < (1 << NR); ++e) {
+      if (((e >> P) & 1) || ((e >> Q) & 1) != V) continue;
+      const vec2_t<R> t = a[e];
+      a[e] = a[e | (1 << P)];
+      a[e | (1 << P)] = t;
+    }
+  }
+}
+
+// the fast-path op set (every op of the random-circuit workloads): returns
+// false for OPC_GENERIC so the caller can interpret it
+template <typename R, int NR>
+__device__ __forceinline__ bool fast_op(const KOp<R>* __restrict__ op, uint32_t opc, vec2_t<R> (&a)[1 << NR],
+                                        uint64_t gthr) {
+  switch (opc) {
+#define SK_FM(P)                                                                              \
+  case OPC_MAT + P:                                                                           \
+    if (P < NR) mat_full<R, NR, (P < NR ? P : 0)>(a, op);                                     \
+    return true;                                                                              \
+  case OPC_MATT + P:                                                                          \
+    if (P < NR && (gthr & op->tmask) == op->tval) mat_full<R, NR, (P < NR ? P : 0)>(a, op); \
+    return true;                                                                              \
+  case OPC_SWAPT + P:                                                                         \
+    if (P < NR && (gthr & op->tmask) == op->tval) swap_slot<R, NR, (P < NR ? P : 0)>(a);    \
+    return true;
+    SK_FM(0) SK_FM(1) SK_FM(2) SK_FM(3)
+#undef SK_FM
+#define SK_FQ(P, Q, V)                                                                  \
+  case OPC_MATQ + 2 * (4 * P + Q) + V:                                                  \
+    if ((gthr & op->tmask) == op->tval) mat_q<R, NR, P, Q, V>(a, op);                   \
+    return true;                                                                        \
+  case OPC_SWAPQ + 2 * (4 * P + Q) + V:                                                 \
+    if ((gthr & op->tmask) == op->tval) swap_q<R, NR, P, Q, V>(a);                      \
+    return true;
+#define SK_FQ2(P, Q) SK_FQ(P, Q, 0) SK_FQ(P, Q, 1)
+    SK_FQ2(0, 1) SK_FQ2(0, 2) SK_FQ2(0, 3) SK_FQ2(1, 0) SK_FQ2(1, 2) SK_FQ2(1, 3)
+    SK_FQ2(2, 0) SK_FQ2(2, 1) SK_FQ2(2, 3) SK_FQ2(3, 0) SK_FQ2(3, 1) SK_FQ2(3, 2)
+#undef SK_FQ2
+#undef SK_FQ
+    case OPC_PHASE: {
+      if ((gthr & op->tmask) != op->tval) return true;
+      const vec2_t<R> c0 = __ldg(reinterpret_cast<const vec2_t<R>*>(op->m));
+      const vec2_t<R> c1 = __ldg(reinterpret_cast<const vec2_t<R>*>(op->m) + 1);
+      const vec2_t<R> c = (gthr & op->qmask) ? c1 : c0;
+      phase_dispatch<R, NR>(op->h.pat, a, c);
+      return true;
+    }
+    default:
+      return false;
+  }
+}
+
 // Generic fused sweep (random circuits, mixed gate streams): NS compile-time
 // stages with per-thread index parts from the host-built table `thr`
 // (uint4 per stage and thread: global bits lo/hi, swizzled shared offset),
 // ops interpreted from `ops` with warp-uniform loads and packed arithmetic.
-template <typename R, int NR, int NS>
+template <typename R, int NR, int NS, bool LEAN>
 __global__ void __launch_bounds__(512, 1) k_sweep(vec2_t<R>* __restrict__ amps, const __grid_constant__ DSweep sw,
                                                   const KOp<R>* __restrict__ ops, const uint4* __restrict__ thr) {
   using V = vec2_t<R>;
@@ -557,31 +647,17 @@ __global__ void __launch_bounds__(512, 1) k_sweep(vec2_t<R>* __restrict__ amps, 
         a[e] = *reinterpret_cast<const V*>(smraw + so);
       }
     }
-    // runs of fast-path ops and of interpreted ops in separate loops, so the
-    // fast loop keeps a[] in fixed registers (one loop with both made ptxas
-    // shuffle all 32 amplitude registers on every iteration)
-    for (int o = st.op_begin; o < st.op_end;) {
-      for (; o < st.op_end; ++o) {
-        const KOp<R>* op = ops + o;
-        const uint32_t opc = op->h.opc;
-        if (opc == OPC_GENERIC) break;
-        switch (opc) {
-#define SK_FM(P)                                                                                \
-  case OPC_MAT + P:                                                                             \
-    if (P < NR) mat_full<R, NR, (P < NR ? P : 0)>(a, op);                                       \
-    break;                                                                                      \
-  case OPC_MATT + P:                                                                            \
-    if (P < NR && (gthr & op->tmask) == op->tval) mat_full<R, NR, (P < NR ? P : 0)>(a, op);   \
-    break;                                                                                      \
-  case OPC_SWAPT + P:                                                                           \
-    if (P < NR && (gthr & op->tmask) == op->tval) swap_slot<R, NR, (P < NR ? P : 0)>(a);      \
-    break;
-          SK_FM(0) SK_FM(1) SK_FM(2) SK_FM(3)
-#undef SK_FM
-          default: break;
-        }
+    if constexpr (LEAN) {  // every op of the sweep has a fast path: no interpreter in the loop
+      for (int o = st.op_begin; o < st.op_end; ++o) fast_op<R, NR>(ops + o, ops[o].h.opc, a, gthr);
+    } else {
+      // runs of fast-path ops and of interpreted ops in separate loops, so the
+      // fast loop keeps a[] in fixed registers (one loop with both made ptxas
+      // shuffle all 32 amplitude registers on every iteration)
+      for (int o = st.op_begin; o < st.op_end;) {
+        for (; o < st.op_end; ++o)
+          if (!fast_op<R, NR>(ops + o, ops[o].h.opc, a, gthr)) break;
+        for (; o < st.op_end && ops[o].h.opc == OPC_GENERIC; ++o) apply_kop<R, NR>(ops + o, a, gthr);
       }
-      for (; o < st.op_end && ops[o].h.opc == OPC_GENERIC; ++o) apply_kop<R, NR>(ops + o, a, gthr);
     }
     if (s == NS - 1) {
       char* p = reinterpret_cast<char*>(amps + gthr);
@@ -1103,11 +1179,18 @@ static int lower_op(const StageCtx& c, const sk_op& op, int o, int width, std::v
 }
 
 static uint32_t opcode_of(const HostKOp& k) {
+  if (k.nr > 4) return OPC_GENERIC;
+  if (k.kind == K_PHASE && k.pat >= 0 && !(k.flags & ~(uint32_t)(F_TPRED | F_QMASK))) return OPC_PHASE;
   if (k.slot < 0 || k.slot >= k.nr || (k.flags & ~(uint32_t)F_TPRED)) return OPC_GENERIC;
-  if (k.emask != slot_mask(k.nr, k.slot, 0)) return OPC_GENERIC;
+  const bool swap = k.kind == K_MATR && k.m[0] == 0 && k.m[2] == 1 && k.m[4] == 1 && k.m[6] == 0;
+  if (k.kind != K_MAT && !swap) return OPC_GENERIC;
   const bool tp = (k.flags & F_TPRED) != 0;
-  if (k.kind == K_MAT) return (tp ? OPC_MATT : OPC_MAT) + k.slot;
-  if (k.kind == K_MATR && k.m[0] == 0 && k.m[2] == 1 && k.m[4] == 1 && k.m[6] == 0) return OPC_SWAPT + k.slot;
+  const uint32_t full = slot_mask(k.nr, k.slot, 0);
+  if (k.emask == full) return swap ? OPC_SWAPT + k.slot : (tp ? OPC_MATT : OPC_MAT) + k.slot;
+  for (int q = 0; q < k.nr; ++q)  // one register-side control
+    for (int v = 0; v < 2; ++v)
+      if (q != k.slot && k.emask == (full & slot_mask(k.nr, q, v)))
+        return (swap ? OPC_SWAPQ : OPC_MATQ) + 2 * (4 * k.slot + q) + v;
   return OPC_GENERIC;
 }
 
@@ -1214,6 +1297,15 @@ struct sk_program {
 
 using namespace sk;
 
+// SK_LEAN_KERNEL=0 keeps the interpreter in every generic sweep (A/B timing)
+static bool use_lean_kernel() {
+  static const int v = [] {
+    const char* e = std::getenv("SK_LEAN_KERNEL");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v != 0;
+}
+
 // SK_QFT_KERNEL=0 runs QFT windows through the generic k_sweep (A/B timing)
 static bool use_qft_kernel() {
   static const int v = [] {
@@ -1229,9 +1321,12 @@ static int launch_one(sk_state* s, const sk_program* p, int i, DevCtx* c) {
   if (!attr_set[s->device]) {
 #define SK_ATTR(K) SK_CUDA(cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024))
     if constexpr (NR <= 4) {
-      SK_ATTR((k_sweep<R, NR, 1>)); SK_ATTR((k_sweep<R, NR, 2>)); SK_ATTR((k_sweep<R, NR, 3>));
-      SK_ATTR((k_sweep<R, NR, 4>)); SK_ATTR((k_sweep<R, NR, 5>)); SK_ATTR((k_sweep<R, NR, 6>));
-      SK_ATTR((k_sweep<R, NR, 7>)); SK_ATTR((k_sweep<R, NR, 8>));
+      SK_ATTR((k_sweep<R, NR, 1, false>)); SK_ATTR((k_sweep<R, NR, 2, false>)); SK_ATTR((k_sweep<R, NR, 3, false>));
+      SK_ATTR((k_sweep<R, NR, 4, false>)); SK_ATTR((k_sweep<R, NR, 5, false>)); SK_ATTR((k_sweep<R, NR, 6, false>));
+      SK_ATTR((k_sweep<R, NR, 7, false>)); SK_ATTR((k_sweep<R, NR, 8, false>));
+      SK_ATTR((k_sweep<R, NR, 1, true>)); SK_ATTR((k_sweep<R, NR, 2, true>)); SK_ATTR((k_sweep<R, NR, 3, true>));
+      SK_ATTR((k_sweep<R, NR, 4, true>)); SK_ATTR((k_sweep<R, NR, 5, true>)); SK_ATTR((k_sweep<R, NR, 6, true>));
+      SK_ATTR((k_sweep<R, NR, 7, true>)); SK_ATTR((k_sweep<R, NR, 8, true>));
     }
     SK_ATTR((k_qft<R, NR, 1>)); SK_ATTR((k_qft<R, NR, 2>)); SK_ATTR((k_qft<R, NR, 3>));
     SK_ATTR((k_qft<R, NR, 4>)); SK_ATTR((k_qft<R, NR, 5>)); SK_ATTR((k_qft<R, NR, 6>));
@@ -1259,9 +1354,12 @@ static int launch_one(sk_state* s, const sk_program* p, int i, DevCtx* c) {
   } else {
     const KOp<R>* ops = (const KOp<R>*)p->d_ops;
     const uint4* thr = (const uint4*)p->d_thr + p->thr_off[i];
-    switch (d.nstages) {
-#define SK_GS(NS_) \
-  case NS_: k_sweep<R, NR, NS_><<<(unsigned)tiles, threads, smem, c->stream>>>(d_amps, d, ops, thr); break;
+    switch (d.nstages * 2 + (d.lean && use_lean_kernel() ? 1 : 0)) {
+#define SK_GS(NS_)                                                                                          \
+  case 2 * NS_: k_sweep<R, NR, NS_, false><<<(unsigned)tiles, threads, smem, c->stream>>>(d_amps, d, ops, thr); \
+    break;                                                                                                  \
+  case 2 * NS_ + 1: k_sweep<R, NR, NS_, true><<<(unsigned)tiles, threads, smem, c->stream>>>(d_amps, d, ops, thr); \
+    break;
       SK_GS(1) SK_GS(2) SK_GS(3) SK_GS(4) SK_GS(5) SK_GS(6) SK_GS(7) SK_GS(8)
 #undef SK_GS
       default: return set_error(SK_EVALUE, "sweep %d: %d stages", i, d.nstages);
@@ -1406,6 +1504,12 @@ int sk_program_create(int width, int dtype, int device, const sk_sweep* sweeps, 
     pack_kops<float>(kops, buf);
   else
     pack_kops<double>(kops, buf);
+  for (auto& d : dsw) {  // pack_kops resolved the phase patterns the opcodes depend on
+    d.lean = d.nr <= 4;
+    for (int st = 0; st < d.nstages; ++st)
+      for (int o = d.st[st].op_begin; o < d.st[st].op_end; ++o)
+        if (opcode_of(kops[o]) == OPC_GENERIC) d.lean = 0;
+  }
   sk_program* prog = new sk_program();
   prog->width = width;
   prog->dtype = dtype;
