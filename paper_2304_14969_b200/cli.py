@@ -13,8 +13,13 @@ fused sweeps, HBM GB/s and the fraction of the measured HBM peak.
 `qft-bench --engine hybrid` times the reference's own path (HybridState on
 |0..0> or GHZ input, cli.py:87-98); `--engine fused` times the fused dense
 executor on a resident state.  Verification uses the QFT's closed forms on
-sampled amplitudes (|0> -> uniform; GHZ -> (1 + e^{-2 pi i j/N}) / sqrt(2N)),
-so it runs at every width.  The `run` subcommand (circuit text files) is out
+sampled amplitudes (|0> -> uniform; GHZ -> (1 + e^{-2 pi i j/N}) / sqrt(2N)):
+for the fused engine at every width (relative tolerance), for the hybrid
+engine with the reference's rule (<= 2^22 amplitudes, 1e-9 absolute).  Like
+the reference, the hybrid engine on GHZ input fails that rule from 18 qubits
+on: its exact-split test (eps <= 1e-10, engine.py:455-460) splits nearly
+separable qubits, an O(sqrt(eps)) amplitude error — ours reproduces the
+reference's 3.310e-08 (n=18) and 3.511e-08 (n=19) with the same splits.  The `run` subcommand (circuit text files) is out
 of scope with the text format.
 """
 from __future__ import annotations
@@ -33,6 +38,7 @@ import numpy as np
 from . import RNG_ALGORITHM, __version__ as VERSION
 
 DEFAULT_BUDGET = 1 << 26  # the reference's DENSE_BUDGET (validate.py:22)
+ORACLE_BUDGET = 1 << 22  # cli.py:39: above this the hybrid run is not verified
 SWEEP_CSV_HEADER = "width,depth,seed,p,f_model,f_exact,wall_ms,peak_amplitudes"  # validate.py:166
 
 
@@ -123,7 +129,8 @@ def cmd_qft_bench(args) -> int:
                 if rep > 0:
                     times.append(time.monotonic() - t0)
             peak_amps = sim.peak_amplitudes
-            ket = sim.full_ket() if (1 << n) <= args.mem_budget else None
+            # the reference's rule (cli.py:100-109): verify up to 2^22 amplitudes at 1e-9 absolute
+            ket = sim.full_ket() if (1 << n) <= min(ORACLE_BUDGET, args.mem_budget) else None
             err = _verify(ket.amplitude, n, args.init, args.dtype) if ket is not None else None
         else:
             if (1 << n) > args.mem_budget:
@@ -151,7 +158,8 @@ def cmd_qft_bench(args) -> int:
             g = moved / statistics.median(times) / 1e9
             gbs, frac = f"{g:.1f}", f"{g / peak:.3f}"
         wall_ms = statistics.median(times) * 1000
-        verified = "" if err is None else ("1" if err < rel_tol * 2.0 ** (-n / 2) else "0")
+        limit = 1e-9 if args.engine == "hybrid" else rel_tol * 2.0 ** (-n / 2)
+        verified = "" if err is None else ("1" if err < limit else "0")
         if verified == "0":
             report.notes.append(f"n={n}: closed-form mismatch {err:.3e}")
         report.rows.append(f"{n},{args.init},{wall_ms:.3f},{peak_amps},{verified},{args.engine},{sweeps},{gbs},{frac}")
