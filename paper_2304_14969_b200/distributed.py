@@ -105,12 +105,39 @@ def emulate(slabs: list[np.ndarray], dtype: str = "c64") -> list[np.ndarray]:
     return cur
 
 
-class ShardedQFT:
-    """Device execution on one rank: two torch buffers (the state and the
-    exchange target) wrapped as sk_state views; NCCL all_to_all_single for
-    the exchanges; fused sweeps for the local work."""
+def pairwise_exchange(dist, buf, staging, world: int, rank: int, group=None) -> None:
+    """In-place all_to_all_single on equal blocks (out[r] block s = in[s]
+    block r) as W-1 pairwise swaps: at step k rank r swaps its block r^k with
+    the partner's block r, chunk by chunk through `staging` (any size).  The
+    whole exchange needs one slab plus the staging buffer instead of two
+    slabs, which is what lets QFT-37 (2^34 amplitudes = 128 GiB per GPU)
+    fit on 8 x 180 GB."""
+    blocks = buf.view(world, -1)
+    csz = min(staging.numel(), blocks.shape[1])
+    for k in range(1, world):
+        partner = rank ^ k
+        blk = blocks[partner]
+        for off in range(0, blk.numel(), csz):
+            n = min(csz, blk.numel() - off)
+            piece, into = blk[off:off + n], staging[:n]
+            ops = [dist.P2POp(dist.isend, piece, partner, group), dist.P2POp(dist.irecv, into, partner, group)]
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+            piece.copy_(into)
 
-    def __init__(self, n_local: int, dtype: str = "c64", group=None):
+
+class ShardedQFT:
+    """Device execution on one rank: the slab (and, for the double-buffered
+    exchange, a second one) as torch buffers wrapped as sk_state views;
+    NCCL all_to_all_single or in-place pairwise NCCL send/recv for the
+    exchanges; fused sweeps for the local work.
+
+    exchange="auto" picks the double-buffered all-to-all when two slabs fit in
+    device memory and the in-place pairwise exchange (one slab + a
+    `chunk_bytes` staging buffer) otherwise."""
+
+    def __init__(self, n_local: int, dtype: str = "c64", group=None, exchange: str = "auto",
+                 chunk_bytes: int = 1 << 30):
         import torch
         import torch.distributed as dist
 
@@ -122,7 +149,19 @@ class ShardedQFT:
         self.n, self.G = layout(n_local, self.world)
         self.device = torch.cuda.current_device()
         real = torch.float32 if dtype == "c64" else torch.float64
-        self.bufs = [torch.empty(2 << n_local, dtype=real, device=f"cuda:{self.device}") for _ in range(2)]
+        slab_bytes = (1 << n_local) * (8 if dtype == "c64" else 16)
+        if exchange == "auto":
+            free, _ = torch.cuda.mem_get_info(self.device)
+            exchange = "alltoall" if (self.G == 0 or 2 * slab_bytes + (4 << 30) <= free) else "pairwise"
+        if exchange not in ("alltoall", "pairwise"):
+            raise ValueError(f"exchange must be 'auto', 'alltoall' or 'pairwise', got {exchange!r}")
+        self.exchange = exchange
+        nbuf = 2 if (exchange == "alltoall" and self.G) else 1
+        self.bufs = [torch.empty(2 << n_local, dtype=real, device=f"cuda:{self.device}") for _ in range(nbuf)]
+        self.staging = None
+        if exchange == "pairwise" and self.G:
+            n_stage = min((2 << n_local) // self.world, max(2, chunk_bytes // real.itemsize))
+            self.staging = torch.empty(n_stage, dtype=real, device=f"cuda:{self.device}")
         self.cur = 0
         h = C.c_void_p()
         _lib.call("sk_wrap", n_local, _lib.DTYPES[dtype], self.device, self.bufs[0].data_ptr(), C.byref(h))
@@ -141,6 +180,9 @@ class ShardedQFT:
         return self.bufs[self.cur]
 
     def _exchange(self):
+        if self.exchange == "pairwise":
+            pairwise_exchange(self.dist, self.bufs[0], self.staging, self.world, self.rank, self.group)
+            return
         nxt = 1 - self.cur
         self.dist.all_to_all_single(self.bufs[nxt], self.bufs[self.cur], group=self.group)
         self.cur = nxt
