@@ -177,7 +177,7 @@ def run_ours(args, rank: int, world: int):
 
     # random normalised global state, generated on the device per rank (not timed)
     g = torch.Generator(device=f"cuda:{dev}").manual_seed(1234 + rank)
-    sq.state.copy_(torch.randn(2 << n_local, device=f"cuda:{dev}", dtype=real, generator=g))
+    sq.state.normal_(generator=g)  # in place: no second slab at 34 qubits
     sq.state.div_(torch.linalg.vector_norm(sq.state) * math.sqrt(world))
     torch.cuda.synchronize()
 
@@ -316,7 +316,7 @@ def run_ours(args, rank: int, world: int):
                                    f"{'s, global-qubit sharded' if world > 1 else ''}); BASELINE configs[1] at N=1",
                        "qubits": n, "qubits_per_gpu": n_local, "state_bytes_per_gpu": slab_bytes,
                        "input": "random normalised state, device-generated",
-                       "l2": "state (1 GiB per GPU) > L2 (126 MB): no flush needed",
+                       "l2": f"state ({slab_bytes / 2**30:g} GiB per GPU) > L2 (126 MB): no flush needed",
                        "swaps": "label permutations (engine.py:525-535)",
                        "parallelism": f"global-qubit sharding over {world} GPUs (2 NCCL all-to-alls per QFT)"
                                       if world > 1 else "single GPU"},
