@@ -72,6 +72,8 @@ int ctx_get(int device, DevCtx** out) {
   return SK_OK;
 }
 
+constexpr int kSmallAmps = 16;
+
 int state_alloc(int width, int dtype, int device, sk_state** out) {
   if (width < 1) return set_error(SK_EVALUE, "shard width must be >= 1");
   if (width > 40) return set_error(SK_EVALUE, "width %d exceeds 40", width);
@@ -86,7 +88,10 @@ int state_alloc(int width, int dtype, int device, sk_state** out) {
   s->elem = elem_size(dtype);
   size_t bytes = (size_t)s->n * s->elem;
   size_t free_b = 0, total_b = 0;
-  if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && bytes > free_b + (size_t(1) << 30)) {
+  // the cudaMemGetInfo pre-check is a ~100 us driver call: only for large
+  // states (small failing allocations still map to SK_ENOMEM below)
+  if (bytes > (size_t(64) << 20) && cudaMemGetInfo(&free_b, &total_b) == cudaSuccess &&
+      bytes > free_b + (size_t(1) << 30)) {
     // pre-check (pool may hold reusable memory, so allow 1 GiB slack)
     cudaError_t e = cudaMallocAsync(&s->d, bytes, c->stream);
     if (e != cudaSuccess) {
@@ -105,6 +110,18 @@ int state_alloc(int width, int dtype, int device, sk_state** out) {
   }
   *out = s;
   return SK_OK;
+}
+
+// tiny shards (the engine's width-1 qubits, engine.py:187-200) travel as a
+// kernel argument: no staging copy and no host wait
+struct SmallAmps {
+  double v[2 * kSmallAmps];
+};
+
+template <typename R>
+__global__ void k_set_small(vec2_t<R>* d, int n, const __grid_constant__ SmallAmps a) {
+  const int i = threadIdx.x;
+  if (i < n) d[i] = mk<R>((R)a.v[2 * i], (R)a.v[2 * i + 1]);
 }
 
 // ---------------------------------------------------------------------------
@@ -810,6 +827,23 @@ int sk_copy_to_device(const sk_state* s, uint64_t dst, int64_t n) {
 int sk_create_from(int width, int dtype, int device, const double* host, sk_state** out) {
   sk_state* s;
   SK_TRY(state_alloc(width, dtype, device, &s));
+  if (s->n <= kSmallAmps) {
+    sk::SmallAmps a{};
+    for (int64_t i = 0; i < 2 * s->n; ++i) a.v[i] = host[i];
+    DevCtx* c;
+    SK_TRY(ctx_get(device, &c));
+    if (dtype == SK_C64)
+      sk::k_set_small<float><<<1, kSmallAmps, 0, c->stream>>>((float2*)s->d, (int)s->n, a);
+    else
+      sk::k_set_small<double><<<1, kSmallAmps, 0, c->stream>>>((double2*)s->d, (int)s->n, a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      sk_destroy(s);
+      return set_error(SK_ECUDA, "k_set_small: %s", cudaGetErrorString(e));
+    }
+    *out = s;
+    return SK_OK;
+  }
   int rc = sk_upload(s, host, s->n);
   if (rc != SK_OK) {
     std::string keep = g_err;
