@@ -13,13 +13,16 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
 tag = sys.argv[1]
-rep = Path(sys.argv[2]) if len(sys.argv) > 2 else ROOT / "gpurun_out" / "prof.ncu-rep"
+rep = Path(sys.argv[2]) if len(sys.argv) > 2 else ROOT / "gpurun_out" / "prof_raw.csv"
 launches = Path(sys.argv[3]) if len(sys.argv) > 3 else ROOT / "gpurun_out" / "launches.csv"
 bench = Path(sys.argv[4]) if len(sys.argv) > 4 else ROOT / "gpurun_out" / "bench.json"
 out = ROOT / "profiles"
 out.mkdir(exist_ok=True)
 
-raw = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+if rep.suffix == ".csv":  # raw page exported on the GPU box
+    raw = rep.read_text()
+else:
+    raw = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 h, units = rows[0], rows[1]
 keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
