@@ -181,23 +181,11 @@ def run_ours(args, rank: int, world: int):
     sq.state.div_(torch.linalg.vector_norm(sq.state) * math.sqrt(world))
     torch.cuda.synchronize()
 
-    body, top = sq.body, sq.top
+    body = sq.body
     nb = body.n_sweeps
 
     def step(evs=None):
-        if G:
-            sq._exchange()
-            _lib.call("sk_rebind", sq._h, sq.state.data_ptr())
-            _lib.call("sk_program_run", sq._h, top._h, 0, -1)
-            sq._exchange()
-        _lib.call("sk_rebind", sq._h, sq.state.data_ptr())
-        if evs is None:
-            _lib.call("sk_program_run", sq._h, body._h, 0, -1)
-        else:
-            evs[0].record(stream)
-            for i in range(nb):
-                _lib.call("sk_program_run", sq._h, body._h, i, 1)
-                evs[i + 1].record(stream)
+        sq.run(evs, stream)
 
     def barrier():
         if dist is not None:
@@ -318,7 +306,8 @@ def run_ours(args, rank: int, world: int):
                        "input": "random normalised state, device-generated",
                        "l2": f"state ({slab_bytes / 2**30:g} GiB per GPU) > L2 (126 MB): no flush needed",
                        "swaps": "label permutations (engine.py:525-535)",
-                       "parallelism": f"global-qubit sharding over {world} GPUs (2 NCCL all-to-alls per QFT)"
+                       "parallelism": f"global-qubit sharding over {world} GPUs ({sq.schedule}-exchange schedule: "
+                                      f"{1 if sq.schedule == 'one' else 2} NCCL all-to-all(s) per QFT, {sq.exchange})"
                                       if world > 1 else "single GPU"},
             "qft_sec": ms_per_step / 1e3,
             "qft_qubits": n,

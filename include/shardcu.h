@@ -208,6 +208,11 @@ int sk_program_lower(int width, int dtype, const sk_sweep* sweeps, int nsweeps, 
 /* Run sweeps [first, first+count) of the program on s (count < 0: all). */
 int sk_program_run(sk_state* s, const sk_program* p, int first, int count);
 int sk_program_nsweeps(const sk_program* p, int* n);
+/* Sharded QFT (no reference counterpart): run a QFT-window
+ * program planned for an (n-G)-qubit shard as the top n-G layers of an
+ * n-qubit QFT whose low G qubits are fixed to `value` on this rank (their
+ * controlled phases fold into the windows' twiddles).  shift = G; 0 clears. */
+int sk_program_set_phase_index(sk_program* p, int shift, uint64_t value);
 
 #ifdef __cplusplus
 }

@@ -86,6 +86,7 @@ _SIGS = {
                          C.POINTER(C.c_int64), C.POINTER(C.c_double), C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)],
     "sk_program_run": [p_state, p_prog, C.c_int, C.c_int],
     "sk_program_nsweeps": [p_prog, C.POINTER(C.c_int)],
+    "sk_program_set_phase_index": [p_prog, C.c_int, C.c_uint64],
 }
 _RESTYPES = {"sk_last_error": C.c_char_p}
 

@@ -711,6 +711,8 @@ struct QStage {
 // a bit-deposit.
 struct QSweep {
   int ntile, nstages, nb, nthreads;
+  int pshift, pad3;  // phase index = (address index << pshift) | pconst (a shard whose low
+  uint64_t pconst;   // pshift QFT qubits are rank constants; 0 / 0 otherwise)
   Run brun[kQRuns];
   const uint4* thr;  // [nstages][nthreads]
   QStage st[kMaxS];
@@ -866,7 +868,7 @@ __global__ void __launch_bounds__(qft_max_threads<R, NR>(), 2) k_qft(vec2_t<R>* 
     }
     switch (st.code) {
 #define SK_QC(L, TOP) \
-  case L * 8 + TOP: pk_chunk<R, NR, L, TOP>(st, a, gthr); break;
+  case L * 8 + TOP: pk_chunk<R, NR, L, TOP>(st, a, (gthr << sw.pshift) | sw.pconst); break;
       SK_QC(1, 0) SK_QC(1, 1) SK_QC(1, 2) SK_QC(1, 3) SK_QC(1, 4)
       SK_QC(2, 1) SK_QC(2, 2) SK_QC(2, 3) SK_QC(2, 4)
       SK_QC(3, 2) SK_QC(3, 3) SK_QC(3, 4)
@@ -1230,6 +1232,28 @@ static uint64_t deposit_h(uint64_t x, const Run* r, int n) {
   return o;
 }
 
+// QFT-window sweep of an (n-G)-qubit shard whose index is the top of an
+// n-qubit QFT register with the low G qubits fixed to `value` (the rank's
+// bits): every phase-space mask and bit position moves up by G, and the
+// bottom window's deferred below-window phase (the CP fans from the G
+// constant qubits) switches on.
+static QSweep phase_shifted(const QSweep& q, int G, uint64_t value) {
+  QSweep o = q;
+  o.pshift = G;
+  o.pconst = value;
+  const uint64_t low = G >= 64 ? ~0ull : ((1ull << G) - 1);
+  for (int s = 0; s < o.nstages; ++s) {
+    QStage& st = o.st[s];
+    if (!st.code) continue;
+    st.tmask <<= G;
+    st.tval <<= G;
+    st.qmask = (st.qmask << G) | low;
+    st.lo += G;
+    if ((st.flags & F_SCALE) && G > 0) st.flags |= F_END;
+  }
+  return o;
+}
+
 // per-thread index table of a sweep: [stage][thread] = {global bits lo, hi,
 // swizzled shared-memory byte offset, 0}
 static void append_thr(const DSweep& d, size_t esz, std::vector<uint4>& thr) {
@@ -1291,6 +1315,8 @@ struct sk_program {
   std::vector<char> qft_ok;
   std::vector<size_t> thr_off;  // per sweep: offset of its per-thread table in d_thr (uint4 units)
   void* d_thr = nullptr;  // per-thread index tables
+  int pshift = 0;         // sk_program_set_phase_index
+  uint64_t pconst = 0;
   void* d_ops = nullptr;
   int nkops = 0;
 };
@@ -1341,7 +1367,7 @@ static int launch_one(sk_state* s, const sk_program* p, int i, DevCtx* c) {
   if (tiles > 0x7fffffffull) return set_error(SK_EVALUE, "too many tiles (%d bits outside the tile)", s->width - T);
   vec2_t<R>* d_amps = (vec2_t<R>*)s->d;
   if (p->qft_ok[i] && threads <= (unsigned)qft_max_threads<R, NR>() && (NR > 4 || use_qft_kernel())) {
-    const QSweep& q = p->qsweeps[i];
+    const QSweep q = p->pshift ? phase_shifted(p->qsweeps[i], p->pshift, p->pconst) : p->qsweeps[i];
     switch (q.nstages) {
 #define SK_QS(NS_) \
   case NS_: k_qft<R, NR, NS_><<<(unsigned)tiles, threads, smem, c->stream>>>(d_amps, q); break;
@@ -1351,6 +1377,8 @@ static int launch_one(sk_state* s, const sk_program* p, int i, DevCtx* c) {
     }
   } else if constexpr (NR > 4) {
     return set_error(SK_EVALUE, "sweep %d: %d register bits need the QFT-window kernel", i, NR);
+  } else if (p->pshift) {
+    return set_error(SK_EVALUE, "sweep %d: a phase-index offset needs the QFT-window kernel", i);
   } else {
     const KOp<R>* ops = (const KOp<R>*)p->d_ops;
     const uint4* thr = (const uint4*)p->d_thr + p->thr_off[i];
@@ -1587,6 +1615,17 @@ int sk_program_destroy(sk_program* p) {
     if (p->d_thr) SK_CUDA(cudaFree(p->d_thr));
   }
   delete p;
+  return SK_OK;
+}
+
+int sk_program_set_phase_index(sk_program* p, int shift, uint64_t value) {
+  if (!p) return set_error(SK_EVALUE, "null program");
+  if (shift < 0 || shift > 24 || (shift < 64 && (value >> shift)))
+    return set_error(SK_EVALUE, "bad phase index offset (shift %d, value %llu)", shift, (unsigned long long)value);
+  for (size_t i = 0; i < p->sweeps.size(); ++i)
+    if (shift && !p->qft_ok[i]) return set_error(SK_EVALUE, "sweep %zu is not a QFT-window sweep", i);
+  p->pshift = shift;
+  p->pconst = value;
   return SK_OK;
 }
 

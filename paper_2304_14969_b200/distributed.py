@@ -19,6 +19,18 @@ distributed path; this is the B200-native extension that makes QFT-37 fit on
 The QFT's final SWAP layer stays a label permutation (full bit reversal).
 Exchanges go through torch.distributed (NCCL over NVLink on the box; gloo in
 the CPU tests), on torch buffers wrapped as non-owning sk_state views.
+
+One-exchange schedule (schedule="one", the default).  If instead the rank
+holds the LOW G qubits (rank r owns the amplitudes whose index ends in r;
+local bit b = qubit b + G), the QFT's first n-G layers (targets n-1..G) are
+all local: each rank runs the ordinary (n-G)-qubit FFT-form body with its
+phase index shifted to (i << G) | r, which folds the controlled phases from
+the G rank-constant qubits into the windows' twiddles
+(sk_program_set_phase_index).  One all-to-all then swaps the rank bits with
+the top G local bits, and a single fused sweep runs the last G layers on the
+moved qubits.  Half the NVLink traffic of the two-exchange schedule for the
+same HBM passes.  The result has the high G qubits as rank bits (`one_x_label`
+gives the element -> qubit-index map); the bit reversal stays a label swap.
 """
 from __future__ import annotations
 
@@ -70,6 +82,43 @@ def plans(n_local: int, world: int, rank: int, dtype: str = "c64"):
         return None, body
     top = fusion.plan_ops(top_layer_ops(n_local, G, rank), n_local, dtype)
     return top, body
+
+
+def tail_ops(n_local: int, G: int) -> list[fusion.Op]:
+    """Ops of QFT layers G-1..0 after the exchange of the one-exchange
+    schedule: qubit j < G sits at local bit n_local - G + j; its CP fan comes
+    only from the moved qubits k < j."""
+    from .circuit import Circuit, cp, h
+    base = n_local - G
+    gates = []
+    for j in range(G - 1, -1, -1):
+        gates.append(h(base + j))
+        for k in range(j - 1, -1, -1):
+            gates.append(cp(math.pi / (1 << (j - k)), base + k, base + j))
+    ops, _ = fusion.lower(Circuit(n_local, tuple(gates)))
+    return fusion.fuse_diagonal_runs(ops)
+
+
+def plans_one_exchange(n_local: int, world: int, dtype: str = "c64"):
+    """(body plan, tail plan or None) of the one-exchange schedule; the body
+    runs with phase index (i << G) | rank on every rank."""
+    n, G = layout(n_local, world)
+    body = fusion.plan_qft(n_local, dtype)
+    tail = fusion.plan_ops(tail_ops(n_local, G), n_local, dtype) if G else None
+    return body, tail
+
+
+def one_x_label(n_local: int, G: int) -> np.ndarray:
+    """Qubit-order index (before the QFT's final SWAP layer) of element
+    (rank s, local l) after the one-exchange schedule, as a flat array over
+    s * 2^n_local + l: rank bits = qubits n-G..n-1, local top bits = qubits
+    0..G-1, local bits b < n_local - G = qubit b + G."""
+    n = n_local + G
+    s = np.repeat(np.arange(1 << G, dtype=np.int64), 1 << n_local)
+    l = np.tile(np.arange(1 << n_local, dtype=np.int64), 1 << G)
+    lo = l & ((1 << (n_local - G)) - 1)
+    top = l >> (n_local - G)
+    return (s << (n - G)) | (lo << G) | top
 
 
 def final_order(n: int) -> list[int]:
@@ -137,7 +186,7 @@ class ShardedQFT:
     `chunk_bytes` staging buffer) otherwise."""
 
     def __init__(self, n_local: int, dtype: str = "c64", group=None, exchange: str = "auto",
-                 chunk_bytes: int = 1 << 30):
+                 chunk_bytes: int = 1 << 30, schedule: str = "one"):
         import torch
         import torch.distributed as dist
 
@@ -166,9 +215,20 @@ class ShardedQFT:
         h = C.c_void_p()
         _lib.call("sk_wrap", n_local, _lib.DTYPES[dtype], self.device, self.bufs[0].data_ptr(), C.byref(h))
         self._h = h
-        top, body = plans(n_local, self.world, self.rank, dtype)
-        self.top = Program(top, self.device) if top is not None else None
-        self.body = Program(body, self.device)
+        if schedule not in ("one", "two"):
+            raise ValueError(f"schedule must be 'one' or 'two', got {schedule!r}")
+        self.schedule = schedule
+        self.top = self.tail = None
+        if schedule == "one":
+            body, tail = plans_one_exchange(n_local, self.world, dtype)
+            self.body = Program(body, self.device)
+            if self.G:
+                self.body.set_phase_index(self.G, self.rank)
+                self.tail = Program(tail, self.device)
+        else:
+            top, body = plans(n_local, self.world, self.rank, dtype)
+            self.top = Program(top, self.device) if top is not None else None
+            self.body = Program(body, self.device)
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -187,23 +247,42 @@ class ShardedQFT:
         self.dist.all_to_all_single(self.bufs[nxt], self.bufs[self.cur], group=self.group)
         self.cur = nxt
 
-    def run(self, events=None):
-        """One sharded QFT body on this rank's slab (stream-ordered on the
-        current torch stream; libshardcu must be bound to it)."""
+    def _run_body(self, events=None, stream=None):
+        _lib.call("sk_rebind", self._h, self.state.data_ptr())
+        if events is None:
+            _lib.call("sk_program_run", self._h, self.body._h, 0, -1)
+            return
+        events[0].record(stream)
+        for i in range(self.body.n_sweeps):
+            _lib.call("sk_program_run", self._h, self.body._h, i, 1)
+            events[i + 1].record(stream)
+
+    def run(self, events=None, stream=None):
+        """One sharded QFT on this rank's slab (stream-ordered on the current
+        torch stream; libshardcu must be bound to it).  `events` (n_sweeps+1
+        CUDA events) bracket the body's fused sweeps for per-launch timing."""
+        if self.schedule == "one":
+            self._run_body(events, stream)
+            if self.G:
+                self._exchange()
+                _lib.call("sk_rebind", self._h, self.state.data_ptr())
+                _lib.call("sk_program_run", self._h, self.tail._h, 0, -1)
+            return
         if self.G:
             self._exchange()
             _lib.call("sk_rebind", self._h, self.state.data_ptr())
             _lib.call("sk_program_run", self._h, self.top._h, 0, -1)
             self._exchange()
-        _lib.call("sk_rebind", self._h, self.state.data_ptr())
-        _lib.call("sk_program_run", self._h, self.body._h, 0, -1)
+        self._run_body(events, stream)
 
     def launches(self) -> int:
-        return (self.top.n_sweeps if self.top else 0) + self.body.n_sweeps
+        extra = self.tail if self.schedule == "one" else self.top
+        return (extra.n_sweeps if extra else 0) + self.body.n_sweeps
 
     def exchange_bytes(self) -> int:
-        """Bytes each rank sends per QFT (two all-to-alls, own block stays)."""
+        """Bytes each rank sends per QFT (one or two all-to-alls, own block stays)."""
         if not self.G:
             return 0
         elem = 8 if self.dtype == "c64" else 16
-        return 2 * (self.world - 1) * ((1 << self.n_local) // self.world) * elem
+        per = (self.world - 1) * ((1 << self.n_local) // self.world) * elem
+        return per * (1 if self.schedule == "one" else 2)

@@ -56,6 +56,11 @@ class Program:
                              f"state is width {state.width} {state.dtype}")
         _lib.call("sk_program_run", state._h, self._h, first, count)
 
+    def set_phase_index(self, shift: int, value: int) -> None:
+        """Run as the top layers of a larger QFT whose low `shift` qubits are
+        the constant `value` (one-exchange sharded QFT; QFT-window programs)."""
+        _lib.call("sk_program_set_phase_index", self._h, shift, value)
+
     def run_handle(self, handle, first: int = 0, count: int = -1) -> None:
         """Run on a raw sk_state handle (e.g. an sk_wrap view over a torch /
         NCCL buffer); the C side checks width, dtype and device."""

@@ -194,3 +194,81 @@ def test_gloo_pairwise_inplace_exchange(world):
             if p.is_alive():
                 p.kill()
     assert max(e for _, e in errs) == 0.0
+
+
+@pytest.mark.parametrize("world,n_local", [(2, 6), (4, 8), (8, 9)])
+def test_one_exchange_schedule_emulated(rng, world, n_local):
+    """One-exchange sharded QFT (rank = low G qubits): phase-shifted body on
+    every rank, one all-to-all, the G-layer tail; kernel-op emulation of
+    every sweep (tests/test_kernel_lowering.emulate) equals the DFT."""
+    from test_kernel_lowering import emulate
+    n, G = D.layout(n_local, world)
+    x = random_state(n, rng)
+    body, tail = D.plans_one_exchange(n_local, world, "c128")
+    slabs = [emulate(body, x[r::world].copy(), pshift=G, pconst=r) for r in range(world)]
+    slabs = D.exchange_blocks(slabs)
+    slabs = [emulate(tail, s_.copy()) for s_ in slabs]
+    u = np.empty(1 << n, complex)
+    u[D.one_x_label(n_local, G)] = np.concatenate(slabs)
+    got = O.permute_qubits(u, D.final_order(n))
+    assert np.max(np.abs(got - O.dft_oracle(x))) < 1e-12
+
+
+def _virtual_one_exchange(x: np.ndarray, world: int, dtype: str) -> np.ndarray:
+    """One-exchange schedule with every rank on cuda:0 (real kernels: the
+    phase-shifted k_qft body, the generic tail sweep)."""
+    import ctypes as C
+
+    from paper_2304_14969_b200 import _lib
+    from paper_2304_14969_b200.executor import Program
+
+    n = int(x.size).bit_length() - 1
+    G = world.bit_length() - 1
+    n_local = n - G
+    cplx = np.complex64 if dtype == "c64" else np.complex128
+    slabs = [torch.view_as_real(torch.from_numpy(x[r::world].astype(cplx))).reshape(-1).to("cuda").contiguous()
+             for r in range(world)]
+    torch.cuda.synchronize()
+    _lib.call("sk_set_stream", 0, torch.cuda.current_stream().cuda_stream)
+    body_plan, tail_plan = D.plans_one_exchange(n_local, world, dtype)
+    tail = Program(tail_plan, 0)
+
+    def run(prog, buf):
+        h = C.c_void_p()
+        _lib.call("sk_wrap", n_local, _lib.DTYPES[dtype], 0, buf.data_ptr(), C.byref(h))
+        try:
+            prog.run_handle(h)
+        finally:
+            _lib._lib.sk_destroy(h)
+
+    for r in range(world):
+        body = Program(body_plan, 0)
+        body.set_phase_index(G, r)
+        run(body, slabs[r])
+    blocks = [c.view(world, -1) for c in slabs]
+    slabs = [torch.cat([blocks[s][r] for s in range(world)]).contiguous() for r in range(world)]
+    for r in range(world):
+        run(tail, slabs[r])
+    torch.cuda.synchronize()
+    u = np.empty(1 << n, complex)
+    u[D.one_x_label(n_local, G)] = np.concatenate([torch.view_as_complex(c.view(-1, 2)).cpu().numpy() for c in slabs])
+    return O.permute_qubits(u, D.final_order(n))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,n_local", [(2, 9), (4, 12), (8, 14)])
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_virtual_ranks_one_exchange_on_device(rng, world, n_local, dtype):
+    n, _ = D.layout(n_local, world)
+    x = random_state(n, rng)
+    got = _virtual_one_exchange(x, world, dtype)
+    assert np.max(np.abs(got - O.dft_oracle(x))) < (1e-12 if dtype == "c128" else 1e-5)
+
+
+@pytest.mark.gpu
+def test_virtual_ranks_one_exchange_large_closed_form():
+    n, world = 25, 8  # 2^22 per slab: three-sweep body with the phase shift
+    x = np.zeros(1 << n, complex)
+    x[0] = x[-1] = 2 ** -0.5
+    got = _virtual_one_exchange(x, world, "c64")
+    assert np.max(np.abs(got - O.qft_of_ghz(n, np.arange(1 << n)))) < 1e-5

@@ -90,7 +90,10 @@ def qft_chunk(amps, g, gthr, regs, e_of, slot, lo, nbits, flags, tmask, tval, qm
         amps *= scale
 
 
-def emulate(plan: fusion.Plan, amps: np.ndarray) -> np.ndarray:
+def emulate(plan: fusion.Plan, amps: np.ndarray, pshift: int = 0, pconst: int = 0) -> np.ndarray:
+    """Run the lowered kernel ops in NumPy.  pshift/pconst mirror
+    sk_program_set_phase_index (phase_shifted in csrc/sk_fused.cu): QFT chunk
+    phases see the index (i << pshift) | pconst."""
     I, Rl, stage_ops = lower(plan)
     n = plan.width
     g = np.arange(1 << n, dtype=np.uint64)
@@ -106,7 +109,13 @@ def emulate(plan: fusion.Plan, amps: np.ndarray) -> np.ndarray:
                 kind, slot, pat, emask, flags, lo, nbits, tmask, tval, qmask, turn, fmask = (int(v) for v in I[k])
                 m = Rl[k]
                 if kind == K_QFTS:
-                    qft_chunk(amps, g, gthr, regs, e_of, slot, lo, nbits, flags, tmask, tval, qmask, m[0])
+                    if pshift:
+                        tmask, tval, lo = tmask << pshift, tval << pshift, lo + pshift
+                        qmask = (qmask << pshift) | ((1 << pshift) - 1)
+                        if flags & F_SCALE:
+                            flags |= F_END
+                    gph = (gthr << np.uint64(pshift)) | np.uint64(pconst)
+                    qft_chunk(amps, g, gph, regs, e_of, slot, lo, nbits, flags, tmask, tval, qmask, m[0])
                     continue
                 ok = np.ones(1 << n, dtype=bool)
                 if flags & F_TPRED:
@@ -171,6 +180,28 @@ def test_qft_fft_form_lowering(rng, dtype, n, tile, low):
     assert set(int(v) for v in I[:, 0]) == {K_QFTS}
     got = emulate(plan, x.copy())
     assert np.max(np.abs(got - O.dft_oracle(x))) < 1e-12
+
+
+@pytest.mark.parametrize("n,G", [(9, 1), (11, 2), (13, 3)])
+def test_phase_shifted_qft_windows(rng, n, G):
+    """A QFT-window program for the top n-G qubits, run with phase index
+    (i << G) | r on the slab whose low G qubits equal r, equals layers
+    n-1..G of the n-qubit QFT (H(j) plus every CP onto j) restricted to that
+    slab: the rank-constant CPs fold into the windows' twiddles."""
+    x = random_state(n, rng)
+    want = x.copy()
+    for gt in build_qft(n).gates:
+        if gt.name == "swap":
+            continue
+        j = gt.targets[0]
+        if j < G:
+            break  # layers G-1 .. 0 are the tail, run after the exchange
+        O.dense_run((gt,), want, gate_matrix)
+    plan = fusion.plan_qft(n - G, "c128", tile_bits=min(n - G, 8), low_bits=3)
+    for r in range(1 << G):
+        slab = x[r::1 << G].copy()
+        got = emulate(plan, slab, pshift=G, pconst=r)
+        assert np.max(np.abs(got - want[r::1 << G])) < 1e-12
 
 
 def test_qft_lowering_uses_butterflies_and_folds():
