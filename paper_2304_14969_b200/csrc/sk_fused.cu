@@ -27,6 +27,9 @@
 // tau = exp(2 pi i frac(F * turn / 2^64)), F a bit field of the thread's
 // index, `turn` the RAMP scale in 64-bit fixed-point turns: exact modular
 // arithmetic, then one MUFU sin/cos (fp32) or sincospi (fp64) per thread.
+#include <cuda.h>  // CUtensorMap (types only; the encoder comes via cudaGetDriverEntryPoint)
+#include <cudaTypedefs.h>
+
 #include <cstdlib>
 #include <vector>
 
@@ -711,8 +714,10 @@ struct QStage {
 // a bit-deposit.
 struct QSweep {
   int ntile, nstages, nb, nthreads;
-  int pshift, pad3;  // phase index = (address index << pshift) | pconst (a shard whose low
+  int tma;           // last stage stores the tile with one TMA bulk-tensor copy (see k_qft)
+  int pshift;        // phase index = (address index << pshift) | pconst (a shard whose low
   uint64_t pconst;   // pshift QFT qubits are rank constants; 0 / 0 otherwise)
+  int pad4, pad5;
   Run brun[kQRuns];
   const uint4* thr;  // [nstages][nthreads]
   QStage st[kMaxS];
@@ -832,9 +837,10 @@ template <typename R, int NR>
 constexpr int qft_max_threads() { return (sizeof(R) == 4 && NR <= 4) ? 512 : 256; }
 
 template <typename R, int NR, int NS>
-__global__ void __launch_bounds__(qft_max_threads<R, NR>(), 2) k_qft(vec2_t<R>* __restrict__ amps, const __grid_constant__ QSweep sw) {
+__global__ void __launch_bounds__(qft_max_threads<R, NR>(), 2) k_qft(vec2_t<R>* __restrict__ amps, const __grid_constant__ QSweep sw,
+                                                                    const __grid_constant__ CUtensorMap tmap) {
   using V = vec2_t<R>;
-  extern __shared__ __align__(16) unsigned char smraw[];
+  extern __shared__ __align__(1024) unsigned char smraw[];
   constexpr int NE = 1 << NR;
   const uint32_t tid = threadIdx.x;
   const uint64_t base = deposit_q(blockIdx.x, sw.brun, sw.nb);
@@ -878,15 +884,49 @@ __global__ void __launch_bounds__(qft_max_threads<R, NR>(), 2) k_qft(vec2_t<R>* 
       default: break;
     }
     if (s == NS - 1) {
-      char* p = reinterpret_cast<char*>(amps + gthr);
+      bool done = false;
+      if constexpr (sizeof(V) == 8 && NR == 4) {
+        if (sw.tma) {
+          // The tile is the contiguous index range [base, base + 2^T) and the
+          // registers hold index bits 0..3: each thread owns one 128-byte row
+          // (t.w = its tile-local index).  Rows go to shared memory in the
+          // TMA 128B-swizzle layout (16-byte chunk j of row r at chunk j ^ (r & 7):
+          // 8 consecutive rows cover all 32 banks), then one thread stores the
+          // whole tile with a single bulk-tensor copy.  Replaces the extra
+          // shared-memory round trip that would re-map lanes onto the low bits.
+          const uint32_t row = t.w >> 4;
+          __syncthreads();  // every lane has finished reading this stage's shared-memory input
+          unsigned char* rp = smraw + row * 128u;
 #pragma unroll
-      for (int k = 0; k < NE; ++k) {
-        const int e = k ^ (k >> 1);
-        if (k) {
-          const int b = ctz_c(k);
-          p = ((e >> b) & 1) ? p + st.reg_goff[b] : p - st.reg_goff[b];
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<float4*>(rp + ((j ^ (row & 7)) << 4)) =
+                make_float4(a[2 * j].x, a[2 * j].y, a[2 * j + 1].x, a[2 * j + 1].y);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncthreads();
+          if (tid == 0) {
+            const uint32_t sm = (uint32_t)__cvta_generic_to_shared(smraw);
+            const int32_t y = (int32_t)(base >> 4);
+            asm volatile(
+                "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(&tmap), "r"(0),
+                "r"(y), "r"(sm)
+                : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          }
+          done = true;
         }
-        *reinterpret_cast<V*>(p) = a[e];
+      }
+      if (!done) {
+        char* p = reinterpret_cast<char*>(amps + gthr);
+#pragma unroll
+        for (int k = 0; k < NE; ++k) {
+          const int e = k ^ (k >> 1);
+          if (k) {
+            const int b = ctz_c(k);
+            p = ((e >> b) & 1) ? p + st.reg_goff[b] : p - st.reg_goff[b];
+          }
+          *reinterpret_cast<V*>(p) = a[e];
+        }
       }
     } else {
       if (s > 0) __syncthreads();
@@ -1264,22 +1304,44 @@ static void append_thr(const DSweep& d, size_t esz, std::vector<uint4>& thr) {
       const uint64_t g = deposit_h((uint64_t)t, a.grun, a.ng);
       const uint32_t l = (uint32_t)deposit_h((uint64_t)t, a.lrun, a.nl);
       const uint32_t so = (esz == 8 ? swz<4>(l) : swz<3>(l)) * (uint32_t)esz;
-      thr.push_back(make_uint4((uint32_t)g, (uint32_t)(g >> 32), so, 0u));
+      thr.push_back(make_uint4((uint32_t)g, (uint32_t)(g >> 32), so, l));
     }
   }
 }
 
 // QSweep for k_qft from a lowered QFT-only sweep (at most one K_QFTS op per
 // stage); false = run it through the generic k_sweep
-static bool qsweep_from(const DSweep& d, const std::vector<HostKOp>& kops, QSweep* q) {
+static bool qft_tma_enabled() {  // SK_QFT_TMA=0 keeps the shared-memory store stage (A/B timing)
+  static const int v = [] {
+    const char* e = std::getenv("SK_QFT_TMA");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v != 0;
+}
+
+static bool qsweep_from(const DSweep& d, const std::vector<HostKOp>& kops, size_t esz, QSweep* q) {
   *q = QSweep{};
   if (!d.qft_only || d.nb > kQRuns || d.nstages > kQftMaxStages) return false;
   q->ntile = d.ntile;
   q->nstages = d.nstages;
   q->nb = d.nb;
   q->nthreads = 1 << (d.ntile - d.nr);
+  // TMA store of the tile (c64, 4 register bits): the tile is the contiguous
+  // low bits [0, T) (no tile bits above: brun starts at bit T), the last stage
+  // is an op-less lane re-map and the stage before it holds index bits 0..3
+  // in slots 0..3; the re-map stage is then replaced by the bulk store.
+  if (esz == 8 && d.nr == 4 && d.ntile - 4 <= 8 && d.nstages >= 2 && qft_tma_enabled()) {
+    const DStage& last = d.st[d.nstages - 1];
+    const DStage& prev = d.st[d.nstages - 2];
+    bool ok = last.op_end == last.op_begin && (d.nb == 0 || d.brun[0].dst == d.ntile);
+    for (int p = 0; p < 4; ++p) ok = ok && prev.reg_goff[p] == (8ull << p);
+    if (ok) {
+      q->tma = 1;
+      q->nstages = d.nstages - 1;
+    }
+  }
   for (int i = 0; i < d.nb; ++i) q->brun[i] = d.brun[i];
-  for (int s = 0; s < d.nstages; ++s) {
+  for (int s = 0; s < q->nstages; ++s) {
     const DStage& a = d.st[s];
     QStage& b = q->st[s];
     if (a.op_end - a.op_begin > 1) return false;
@@ -1341,6 +1403,29 @@ static bool use_qft_kernel() {
   return v != 0;
 }
 
+// 2-D tensor map over a c64 state viewed as rows of 16 amplitudes (128 B):
+// box = one tile of 2^T amplitudes (2^(T-4) rows), 128-byte swizzle
+static int tile_store_map(CUtensorMap* m, void* d, int width, int T) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return (PFN_cuTensorMapEncodeTiled_v12000)f;
+  }();
+  if (!enc) return set_error(SK_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[2] = {16, (cuuint64_t)1 << (width - 4)};
+  const cuuint64_t strides[1] = {128};
+  const cuuint32_t box[2] = {16, (cuuint32_t)1 << (T - 4)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, d, dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(SK_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return SK_OK;
+}
+
 template <typename R, int NR>
 static int launch_one(sk_state* s, const sk_program* p, int i, DevCtx* c) {
   static bool attr_set[64] = {false};
@@ -1368,9 +1453,11 @@ static int launch_one(sk_state* s, const sk_program* p, int i, DevCtx* c) {
   vec2_t<R>* d_amps = (vec2_t<R>*)s->d;
   if (p->qft_ok[i] && threads <= (unsigned)qft_max_threads<R, NR>() && (NR > 4 || use_qft_kernel())) {
     const QSweep q = p->pshift ? phase_shifted(p->qsweeps[i], p->pshift, p->pconst) : p->qsweeps[i];
+    CUtensorMap tmap{};
+    if (q.tma) SK_TRY(tile_store_map(&tmap, s->d, s->width, T));
     switch (q.nstages) {
 #define SK_QS(NS_) \
-  case NS_: k_qft<R, NR, NS_><<<(unsigned)tiles, threads, smem, c->stream>>>(d_amps, q); break;
+  case NS_: k_qft<R, NR, NS_><<<(unsigned)tiles, threads, smem, c->stream>>>(d_amps, q, tmap); break;
       SK_QS(1) SK_QS(2) SK_QS(3) SK_QS(4) SK_QS(5) SK_QS(6)
 #undef SK_QS
       default: return set_error(SK_EVALUE, "sweep %d: %d stages", i, q.nstages);
@@ -1550,7 +1637,7 @@ int sk_program_create(int width, int dtype, int device, const sk_sweep* sweeps, 
   for (size_t i = 0; i < dsw.size(); ++i) {
     prog->thr_off[i] = thr.size();
     append_thr(dsw[i], dtype == SK_C64 ? 8 : 16, thr);
-    prog->qft_ok[i] = qsweep_from(dsw[i], kops, &prog->qsweeps[i]);
+    prog->qft_ok[i] = qsweep_from(dsw[i], kops, dtype == SK_C64 ? 8 : 16, &prog->qsweeps[i]);
   }
   if (!thr.empty()) {
     cudaError_t e = cudaMalloc(&prog->d_thr, thr.size() * sizeof(uint4));
