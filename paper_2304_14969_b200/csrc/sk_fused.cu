@@ -885,27 +885,35 @@ __global__ void __launch_bounds__(qft_max_threads<R, NR>(), 2) k_qft(vec2_t<R>* 
     }
     if (s == NS - 1) {
       bool done = false;
-      if constexpr (sizeof(V) == 8 && NR == 4) {
+      if constexpr (NR == 4) {
         if (sw.tma) {
           // The tile is the contiguous index range [base, base + 2^T) and the
-          // registers hold index bits 0..3: each thread owns one 128-byte row
-          // (t.w = its tile-local index).  Rows go to shared memory in the
+          // registers hold index bits 0..3: each thread owns one (c64) or two
+          // (c128) 128-byte rows (t.w = its tile-local index).  Rows go to shared memory in the
           // TMA 128B-swizzle layout (16-byte chunk j of row r at chunk j ^ (r & 7):
           // 8 consecutive rows cover all 32 banks), then one thread stores the
           // whole tile with a single bulk-tensor copy.  Replaces the extra
           // shared-memory round trip that would re-map lanes onto the low bits.
-          const uint32_t row = t.w >> 4;
           __syncthreads();  // every lane has finished reading this stage's shared-memory input
-          unsigned char* rp = smraw + row * 128u;
+          if constexpr (sizeof(V) == 8) {  // c64: one 128-byte row = 16 amplitudes = this thread's registers
+            const uint32_t row = t.w >> 4;
+            unsigned char* rp = smraw + row * 128u;
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            *reinterpret_cast<float4*>(rp + ((j ^ (row & 7)) << 4)) =
-                make_float4(a[2 * j].x, a[2 * j].y, a[2 * j + 1].x, a[2 * j + 1].y);
+            for (int j = 0; j < 8; ++j)
+              *reinterpret_cast<float4*>(rp + ((j ^ (row & 7)) << 4)) =
+                  make_float4(a[2 * j].x, a[2 * j].y, a[2 * j + 1].x, a[2 * j + 1].y);
+          } else {  // c128: two rows of 8 amplitudes, one 16-byte chunk each
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const uint32_t row = (t.w >> 3) + (e >> 3);
+              *reinterpret_cast<V*>(smraw + row * 128u + (((e & 7) ^ (row & 7)) << 4)) = a[e];
+            }
+          }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncthreads();
           if (tid == 0) {
             const uint32_t sm = (uint32_t)__cvta_generic_to_shared(smraw);
-            const int32_t y = (int32_t)(base >> 4);
+            const int32_t y = (int32_t)(base >> (sizeof(V) == 8 ? 4 : 3));
             asm volatile(
                 "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(&tmap), "r"(0),
                 "r"(y), "r"(sm)
@@ -1330,11 +1338,12 @@ static bool qsweep_from(const DSweep& d, const std::vector<HostKOp>& kops, size_
   // low bits [0, T) (no tile bits above: brun starts at bit T), the last stage
   // is an op-less lane re-map and the stage before it holds index bits 0..3
   // in slots 0..3; the re-map stage is then replaced by the bulk store.
-  if (esz == 8 && d.nr == 4 && d.ntile - 4 <= 8 && d.nstages >= 2 && qft_tma_enabled()) {
+  const int row_bits = esz == 8 ? 4 : 3;  // log2 amplitudes per 128-byte row
+  if (d.nr == 4 && d.ntile - row_bits <= 8 && d.nstages >= 2 && qft_tma_enabled()) {
     const DStage& last = d.st[d.nstages - 1];
     const DStage& prev = d.st[d.nstages - 2];
     bool ok = last.op_end == last.op_begin && (d.nb == 0 || d.brun[0].dst == d.ntile);
-    for (int p = 0; p < 4; ++p) ok = ok && prev.reg_goff[p] == (8ull << p);
+    for (int p = 0; p < 4; ++p) ok = ok && prev.reg_goff[p] == ((uint64_t)esz << p);
     if (ok) {
       q->tma = 1;
       q->nstages = d.nstages - 1;
@@ -1403,9 +1412,9 @@ static bool use_qft_kernel() {
   return v != 0;
 }
 
-// 2-D tensor map over a c64 state viewed as rows of 16 amplitudes (128 B):
-// box = one tile of 2^T amplitudes (2^(T-4) rows), 128-byte swizzle
-static int tile_store_map(CUtensorMap* m, void* d, int width, int T) {
+// 2-D tensor map over a state viewed as 128-byte rows (16 c64 or 8 c128
+// amplitudes): box = one tile of 2^T amplitudes, 128-byte swizzle
+static int tile_store_map(CUtensorMap* m, void* d, int width, int T, int row_bits) {
   static PFN_cuTensorMapEncodeTiled_v12000 enc = [] {
     void* f = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -1415,9 +1424,9 @@ static int tile_store_map(CUtensorMap* m, void* d, int width, int T) {
     return (PFN_cuTensorMapEncodeTiled_v12000)f;
   }();
   if (!enc) return set_error(SK_ECUDA, "cuTensorMapEncodeTiled unavailable");
-  const cuuint64_t dims[2] = {16, (cuuint64_t)1 << (width - 4)};
+  const cuuint64_t dims[2] = {16, (cuuint64_t)1 << (width - row_bits)};
   const cuuint64_t strides[1] = {128};
-  const cuuint32_t box[2] = {16, (cuuint32_t)1 << (T - 4)};
+  const cuuint32_t box[2] = {16, (cuuint32_t)1 << (T - row_bits)};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, d, dims, strides, box, estr,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
@@ -1454,7 +1463,7 @@ static int launch_one(sk_state* s, const sk_program* p, int i, DevCtx* c) {
   if (p->qft_ok[i] && threads <= (unsigned)qft_max_threads<R, NR>() && (NR > 4 || use_qft_kernel())) {
     const QSweep q = p->pshift ? phase_shifted(p->qsweeps[i], p->pshift, p->pconst) : p->qsweeps[i];
     CUtensorMap tmap{};
-    if (q.tma) SK_TRY(tile_store_map(&tmap, s->d, s->width, T));
+    if (q.tma) SK_TRY(tile_store_map(&tmap, s->d, s->width, T, sizeof(vec2_t<R>) == 8 ? 4 : 3));
     switch (q.nstages) {
 #define SK_QS(NS_) \
   case NS_: k_qft<R, NR, NS_><<<(unsigned)tiles, threads, smem, c->stream>>>(d_amps, q, tmap); break;
