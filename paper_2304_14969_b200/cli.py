@@ -182,8 +182,7 @@ def _parse_span(text: str) -> list[int]:
 
 
 def cmd_min_sdrp(args) -> int:
-    from .circuit import derive_seed
-    from .sdrp import min_sdrp_search
+    from .sdrp import min_sdrp_ensemble
 
     if args.width >= 54 and not args.i_have_80gb:
         print("error: usage: width >= 54 needs tens of GB of amplitude storage; pass --i-have-80gb to acknowledge",
@@ -193,11 +192,10 @@ def cmd_min_sdrp(args) -> int:
                          "width,depth,seed,p_min,f_model,peak_amplitudes,wall_ms")
     for depth in _parse_span(args.depths):
         values = []
-        for i in range(args.circuits):
-            seed = derive_seed(args.seed, i)
-            t0 = time.monotonic()
-            res = min_sdrp_search(args.width, depth, seed, args.mem_budget, dtype=args.dtype)
-            wall_ms = (time.monotonic() - t0) * 1000
+        results = min_sdrp_ensemble(args.width, depth, args.circuits, args.seed, args.mem_budget,
+                                    workers=args.threads, dtype=args.dtype)
+        for seed, res, wall_s in results:
+            wall_ms = wall_s * 1000
             if not res.feasible:
                 report.rows.append(f"{args.width},{depth},{seed},,,,{wall_ms:.1f}")
                 continue
@@ -207,7 +205,7 @@ def cmd_min_sdrp(args) -> int:
         mean = sum(values) / len(values) if values else None
         shown = "infeasible" if mean is None else f"{mean:.4g}"
         print(f"depth={depth:3d} circuits={len(values)} mean_f_model={shown}")
-    report.write_csv(args.out, args.seed, 1, _device_name(), args.dtype)
+    report.write_csv(args.out, args.seed, args.threads, _device_name(), args.dtype)
     return 0
 
 
@@ -298,6 +296,7 @@ def build_parser() -> argparse.ArgumentParser:
     p.add_argument("--depths", default="1:10", help="lo:hi or comma list")
     p.add_argument("--circuits", type=int, default=100)
     p.add_argument("--i-have-80gb", action="store_true", help="acknowledge the memory cost of width >= 54")
+    p.add_argument("--threads", type=int, default=1, help="worker processes sharing the GPU (validate.py:223-229)")
     _add_common(p, "min_sdrp.csv", "c128")
     p.set_defaults(func=cmd_min_sdrp)
     return ap

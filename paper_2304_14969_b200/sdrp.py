@@ -77,3 +77,33 @@ def min_sdrp_search(width: int, depth: int, seed: int, mem_budget: int, p_step: 
         if p == 0.0:
             break
     return best
+
+
+def _search_worker(args):
+    width, depth, seed, budget, p_step, dtype, device = args
+    from .ket import set_default_device
+    set_default_device(device)
+    t0 = time.perf_counter()
+    r = min_sdrp_search(width, depth, seed, budget, p_step, dtype)
+    return seed, r, time.perf_counter() - t0
+
+
+def min_sdrp_ensemble(width: int, depth: int, n_circuits: int, base_seed: int, mem_budget: int,
+                      workers: int = 1, p_step: float = DEFAULT_P_STEP, dtype: str = "c128",
+                      devices: list[int] | None = None):
+    """min_sdrp_search over circuits derive_seed(base_seed, i), i < n_circuits,
+    spread over `workers` processes (the reference's process-pool sweep,
+    validate.py:203-204,223-229).  The searches are host-bound on the small
+    shards of 54-qubit SDRP, so several processes share one GPU well; with
+    `devices` they are dealt round-robin over GPUs.  Returns
+    [(seed, MinSdrpResult, wall_s)] in circuit order."""
+    from .circuit import derive_seed
+    devices = devices or [0]
+    jobs = [(width, depth, derive_seed(base_seed, i), mem_budget, p_step, dtype, devices[i % len(devices)])
+            for i in range(n_circuits)]
+    if workers <= 1:
+        return [_search_worker(j) for j in jobs]
+    import multiprocessing as mp
+    from concurrent.futures import ProcessPoolExecutor
+    with ProcessPoolExecutor(max_workers=workers, mp_context=mp.get_context("spawn")) as pool:
+        return list(pool.map(_search_worker, jobs))
