@@ -167,3 +167,16 @@ def test_sharded_qft_plans_on_device(world, n_local):
     out = np.concatenate([k.amps for k in slabs])
     got = O.permute_qubits(out, D.final_order(n))
     assert np.max(np.abs(got - O.dft_oracle(x))) < 1e-5
+
+
+def test_phase_index_offset_validation():
+    """sk_program_set_phase_index: QFT-window programs only; value < 2^shift."""
+    from paper_2304_14969_b200 import fusion
+    prog = Program(fusion.plan_qft(12, "c64"))
+    with pytest.raises(ValueError):
+        prog.set_phase_index(2, 4)  # value needs more than 2 bits
+    prog.set_phase_index(2, 3)
+    prog.set_phase_index(0, 0)
+    gen = compile_circuit(build_random_circuit(12, 3, 1), dtype="c64")
+    with pytest.raises(ValueError):
+        gen.set_phase_index(1, 1)  # generic sweeps cannot fold rank-constant phases
