@@ -90,8 +90,7 @@ enum KOpc : uint32_t {
   OPC_MATQ = 16,   // + 2 (4P + Q) + V: dense 2x2 on slot P where register slot Q == V
   OPC_SWAPQ = 48,  // + 2 (4P + Q) + V: X on slot P where register slot Q == V
   OPC_PHASE = 80,  // K_PHASE with a specialised element pattern
-  OPC_MAT2 = 96,   // + 4 P1 + P2: two consecutive unpredicated dense 2x2 (this op on P1, the next on P2)
-  OPC_END = 112
+  OPC_END = 81
 };
 
 template <typename R>
@@ -569,56 +568,44 @@ __device__ __forceinline__ void swap_q(vec2_t<R> (&a)[1 << NR]) {
 
 // the fast-path op set (every op of the random-circuit workloads): returns
 // false for OPC_GENERIC so the caller can interpret it
-// returns the number of ops consumed (2 for OPC_MAT2), 0 for OPC_GENERIC
 template <typename R, int NR>
-__device__ __forceinline__ int fast_op(const KOp<R>* __restrict__ op, uint32_t opc, vec2_t<R> (&a)[1 << NR],
-                                       uint64_t gthr) {
+__device__ __forceinline__ bool fast_op(const KOp<R>* __restrict__ op, uint32_t opc, vec2_t<R> (&a)[1 << NR],
+                                        uint64_t gthr) {
   switch (opc) {
 #define SK_FM(P)                                                                              \
   case OPC_MAT + P:                                                                           \
     if (P < NR) mat_full<R, NR, (P < NR ? P : 0)>(a, op);                                     \
-    return 1;                                                                              \
+    return true;                                                                              \
   case OPC_MATT + P:                                                                          \
     if (P < NR && (gthr & op->tmask) == op->tval) mat_full<R, NR, (P < NR ? P : 0)>(a, op); \
-    return 1;                                                                              \
+    return true;                                                                              \
   case OPC_SWAPT + P:                                                                         \
     if (P < NR && (gthr & op->tmask) == op->tval) swap_slot<R, NR, (P < NR ? P : 0)>(a);    \
-    return 1;
+    return true;
     SK_FM(0) SK_FM(1) SK_FM(2) SK_FM(3)
 #undef SK_FM
 #define SK_FQ(P, Q, V)                                                                  \
   case OPC_MATQ + 2 * (4 * P + Q) + V:                                                  \
     if ((gthr & op->tmask) == op->tval) mat_q<R, NR, P, Q, V>(a, op);                   \
-    return 1;                                                                        \
+    return true;                                                                        \
   case OPC_SWAPQ + 2 * (4 * P + Q) + V:                                                 \
     if ((gthr & op->tmask) == op->tval) swap_q<R, NR, P, Q, V>(a);                      \
-    return 1;
+    return true;
 #define SK_FQ2(P, Q) SK_FQ(P, Q, 0) SK_FQ(P, Q, 1)
     SK_FQ2(0, 1) SK_FQ2(0, 2) SK_FQ2(0, 3) SK_FQ2(1, 0) SK_FQ2(1, 2) SK_FQ2(1, 3)
     SK_FQ2(2, 0) SK_FQ2(2, 1) SK_FQ2(2, 3) SK_FQ2(3, 0) SK_FQ2(3, 1) SK_FQ2(3, 2)
 #undef SK_FQ2
 #undef SK_FQ
-#define SK_F2(P1, P2)                                                  \
-  case OPC_MAT2 + 4 * P1 + P2:                                         \
-    if (P1 < NR && P2 < NR) {                                          \
-      mat_full<R, NR, (P1 < NR ? P1 : 0)>(a, op);                      \
-      mat_full<R, NR, (P2 < NR ? P2 : 0)>(a, op + 1);                  \
-    }                                                                  \
-    return 2;
-#define SK_F2R(P1) SK_F2(P1, 0) SK_F2(P1, 1) SK_F2(P1, 2) SK_F2(P1, 3)
-    SK_F2R(0) SK_F2R(1) SK_F2R(2) SK_F2R(3)
-#undef SK_F2R
-#undef SK_F2
     case OPC_PHASE: {
-      if ((gthr & op->tmask) != op->tval) return 1;
+      if ((gthr & op->tmask) != op->tval) return true;
       const vec2_t<R> c0 = __ldg(reinterpret_cast<const vec2_t<R>*>(op->m));
       const vec2_t<R> c1 = __ldg(reinterpret_cast<const vec2_t<R>*>(op->m) + 1);
       const vec2_t<R> c = (gthr & op->qmask) ? c1 : c0;
       phase_dispatch<R, NR>(op->h.pat, a, c);
-      return 1;
+      return true;
     }
     default:
-      return 0;
+      return false;
   }
 }
 
@@ -664,20 +651,14 @@ __global__ void __launch_bounds__(512, 1) k_sweep(vec2_t<R>* __restrict__ amps, 
       }
     }
     if constexpr (LEAN) {  // every op of the sweep has a fast path: no interpreter in the loop
-      for (int o = st.op_begin; o < st.op_end;) {
-        const int c = fast_op<R, NR>(ops + o, ops[o].h.opc, a, gthr);
-        o += c ? c : 1;
-      }
+      for (int o = st.op_begin; o < st.op_end; ++o) fast_op<R, NR>(ops + o, ops[o].h.opc, a, gthr);
     } else {
       // runs of fast-path ops and of interpreted ops in separate loops, so the
       // fast loop keeps a[] in fixed registers (one loop with both made ptxas
       // shuffle all 32 amplitude registers on every iteration)
       for (int o = st.op_begin; o < st.op_end;) {
-        for (; o < st.op_end;) {
-          const int c = fast_op<R, NR>(ops + o, ops[o].h.opc, a, gthr);
-          if (!c) break;
-          o += c;
-        }
+        for (; o < st.op_end; ++o)
+          if (!fast_op<R, NR>(ops + o, ops[o].h.opc, a, gthr)) break;
         for (; o < st.op_end && ops[o].h.opc == OPC_GENERIC; ++o) apply_kop<R, NR>(ops + o, a, gthr);
       }
     }
@@ -1247,14 +1228,6 @@ static int lower_op(const StageCtx& c, const sk_op& op, int o, int width, std::v
   return set_error(SK_EVALUE, "op %d: unknown kind %d", o, op.kind);
 }
 
-static bool pair_ops_enabled() {  // SK_PAIR_OPS=0: one dispatch per gate (A/B timing)
-  static const int v = [] {
-    const char* e = std::getenv("SK_PAIR_OPS");
-    return e ? std::atoi(e) : 1;
-  }();
-  return v != 0;
-}
-
 static uint32_t opcode_of(const HostKOp& k) {
   if (k.nr > 4) return OPC_GENERIC;
   if (k.kind == K_PHASE && k.pat >= 0 && !(k.flags & ~(uint32_t)(F_TPRED | F_QMASK))) return OPC_PHASE;
@@ -1272,7 +1245,7 @@ static uint32_t opcode_of(const HostKOp& k) {
 }
 
 template <typename R>
-static void pack_kops(std::vector<HostKOp>& h, const std::vector<uint32_t>& opc, std::vector<unsigned char>& buf) {
+static void pack_kops(std::vector<HostKOp>& h, std::vector<unsigned char>& buf) {
   buf.assign(sizeof(KOp<R>) * h.size(), 0);
   KOp<R>* k = reinterpret_cast<KOp<R>*>(buf.data());
   for (size_t i = 0; i < h.size(); ++i) {
@@ -1285,7 +1258,7 @@ static void pack_kops(std::vector<HostKOp>& h, const std::vector<uint32_t>& opc,
     x.h.lo = (uint8_t)h[i].lo;
     x.h.nbits = (uint8_t)h[i].nbits;
     x.h.flags = h[i].flags;
-    x.h.opc = opc[i];
+    x.h.opc = opcode_of(h[i]);
     x.tmask = h[i].tmask;
     x.tval = h[i].tval;
     x.qmask = h[i].qmask;
@@ -1651,31 +1624,16 @@ int sk_program_create(int width, int dtype, int device, const sk_sweep* sweeps, 
   DevCtx* c;
   SK_TRY(ctx_get(device, &c));
   std::vector<unsigned char> buf;
-  for (auto& k : kops)  // the opcodes depend on the phase patterns
-    if (k.kind == K_PHASE || k.kind == K_TPHASE) k.pat = pattern_of(k.nr, k.emask);
-  std::vector<uint32_t> opc(kops.size());
-  for (size_t i = 0; i < kops.size(); ++i) opc[i] = opcode_of(kops[i]);
-  for (auto& d : dsw) {
-    d.lean = d.nr <= 4;
-    for (int st = 0; st < d.nstages; ++st) {
-      for (int o = d.st[st].op_begin; o < d.st[st].op_end; ++o)
-        if (opc[o] == OPC_GENERIC) d.lean = 0;
-      // pair consecutive unpredicated dense 2x2 ops of a stage: one dispatch per two gates
-      for (int o = d.st[st].op_begin; o + 1 < d.st[st].op_end;) {
-        const bool m0 = opc[o] >= OPC_MAT && opc[o] < OPC_MAT + 4, m1 = opc[o + 1] >= OPC_MAT && opc[o + 1] < OPC_MAT + 4;
-        if (m0 && m1 && pair_ops_enabled()) {
-          opc[o] = OPC_MAT2 + 4 * (opc[o] - OPC_MAT) + (opc[o + 1] - OPC_MAT);
-          o += 2;
-        } else {
-          o += 1;
-        }
-      }
-    }
-  }
   if (dtype == SK_C64)
-    pack_kops<float>(kops, opc, buf);
+    pack_kops<float>(kops, buf);
   else
-    pack_kops<double>(kops, opc, buf);
+    pack_kops<double>(kops, buf);
+  for (auto& d : dsw) {  // pack_kops resolved the phase patterns the opcodes depend on
+    d.lean = d.nr <= 4;
+    for (int st = 0; st < d.nstages; ++st)
+      for (int o = d.st[st].op_begin; o < d.st[st].op_end; ++o)
+        if (opcode_of(kops[o]) == OPC_GENERIC) d.lean = 0;
+  }
   sk_program* prog = new sk_program();
   prog->width = width;
   prog->dtype = dtype;
