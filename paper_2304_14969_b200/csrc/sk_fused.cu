@@ -653,14 +653,9 @@ __global__ void __launch_bounds__(512, 1) k_sweep(vec2_t<R>* __restrict__ amps, 
     if constexpr (LEAN) {  // every op of the sweep has a fast path: no interpreter in the loop
       for (int o = st.op_begin; o < st.op_end; ++o) fast_op<R, NR>(ops + o, ops[o].h.opc, a, gthr);
     } else {
-      // runs of fast-path ops and of interpreted ops in separate loops, so the
-      // fast loop keeps a[] in fixed registers (one loop with both made ptxas
-      // shuffle all 32 amplitude registers on every iteration)
-      for (int o = st.op_begin; o < st.op_end;) {
-        for (; o < st.op_end; ++o)
-          if (!fast_op<R, NR>(ops + o, ops[o].h.opc, a, gthr)) break;
-        for (; o < st.op_end && ops[o].h.opc == OPC_GENERIC; ++o) apply_kop<R, NR>(ops + o, a, gthr);
-      }
+      // sweeps with ops outside the fast-path set are interpreted op by op
+      // (inlining the fast-path table here too multiplied nvcc time)
+      for (int o = st.op_begin; o < st.op_end; ++o) apply_kop<R, NR>(ops + o, a, gthr);
     }
     if (s == NS - 1) {
       char* p = reinterpret_cast<char*>(amps + gthr);
@@ -1440,7 +1435,7 @@ static int launch_one(sk_state* s, const sk_program* p, int i, DevCtx* c) {
   static bool attr_set[64] = {false};
   if (!attr_set[s->device]) {
 #define SK_ATTR(K) SK_CUDA(cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024))
-    if constexpr (NR <= 4) {
+    if constexpr (NR <= 4 && !(sizeof(R) == 8 && NR == 4)) {
       SK_ATTR((k_sweep<R, NR, 1, false>)); SK_ATTR((k_sweep<R, NR, 2, false>)); SK_ATTR((k_sweep<R, NR, 3, false>));
       SK_ATTR((k_sweep<R, NR, 4, false>)); SK_ATTR((k_sweep<R, NR, 5, false>)); SK_ATTR((k_sweep<R, NR, 6, false>));
       SK_ATTR((k_sweep<R, NR, 7, false>)); SK_ATTR((k_sweep<R, NR, 8, false>));
@@ -1471,7 +1466,7 @@ static int launch_one(sk_state* s, const sk_program* p, int i, DevCtx* c) {
 #undef SK_QS
       default: return set_error(SK_EVALUE, "sweep %d: %d stages", i, q.nstages);
     }
-  } else if constexpr (NR > 4) {
+  } else if constexpr (NR > 4 || (sizeof(R) == 8 && NR == 4)) {  // 4-bit c128 / 5-bit c64: QFT windows only
     return set_error(SK_EVALUE, "sweep %d: %d register bits need the QFT-window kernel", i, NR);
   } else if (p->pshift) {
     return set_error(SK_EVALUE, "sweep %d: a phase-index offset needs the QFT-window kernel", i);
@@ -1523,11 +1518,11 @@ static int lower_program(int width, int dtype, const sk_sweep* sweeps, int nswee
     const int NR = sw.nreg ? sw.nreg : NR0;
     if (!(NR == 4 || (dtype == SK_C128 && NR == 3) || (dtype == SK_C64 && NR == 5)))
       return set_error(SK_EVALUE, "sweep %d: %d register bits not supported for this dtype", si, NR);
-    if (NR == 5)  // 32-element register sets exist only in the QFT-window kernel
+    if (NR == 5 || (dtype == SK_C128 && NR == 4))  // these register sets exist only in the QFT-window kernel
       for (int s = 0; s < sw.nstages; ++s)
         for (int o = sw.op_begin[s]; o < sw.op_begin[s + 1]; ++o)
           if (o >= 0 && o < nops && ops[o].kind != SK_OP_QFT)
-            return set_error(SK_EVALUE, "sweep %d: 5 register bits are only supported for QFT-window ops", si);
+            return set_error(SK_EVALUE, "sweep %d: %d register bits are only supported for QFT-window ops", si, NR);
     d.nr = NR;
     const int maxT = dtype == SK_C64 ? kMaxTile32 : kMaxTile64;
     const int T = sw.ntile;
