@@ -18,7 +18,9 @@
  *   - 2x2 matrices are `const double m[8]` = re/im of m00, m01, m10, m11.
  *   - every function returns an int status; no C++ exception crosses the ABI.
  *       SK_OK 0, SK_EINDEX -> IndexError, SK_EVALUE -> ValueError,
- *       SK_ENOMEM -> MemoryBudgetError, SK_ECUDA -> RuntimeError.
+ *       SK_ENOMEM -> DeviceMemoryError (the device is out of memory),
+ *       SK_EBUDGET -> MemoryBudgetError (the engine's configured budget),
+ *       SK_ECUDA -> RuntimeError.
  *     sk_last_error() returns a thread-local message for the last failure.
  *   - single writer per state (ket.py:65-66).  All work is ordered on one
  *     CUDA stream per device (sk_set_stream may replace it); functions that
@@ -38,6 +40,7 @@ extern "C" {
 #define SK_EVALUE 2
 #define SK_ENOMEM 3
 #define SK_ECUDA 4
+#define SK_EBUDGET 5 /* the hybrid engine's dense-amplitude budget (engine.py:202-209) */
 
 #define SK_C64 0
 #define SK_C128 1
@@ -213,6 +216,71 @@ int sk_program_nsweeps(const sk_program* p, int* n);
  * n-qubit QFT whose low G qubits are fixed to `value` on this rank (their
  * controlled phases fold into the windows' twiddles).  shift = G; 0 clears. */
 int sk_program_set_phase_index(sk_program* p, int shift, uint64_t value);
+
+/* ---- native hybrid engine (engine.py HybridState, dense shards) ---------
+ * The factorised simulator's commit stream runs in C++ next to the kernels:
+ * 1q buffers, pending controlled-op queues, control elimination, merges,
+ * exact splits and SDRP rounding with the reference's rules
+ * (engine.py:164-784 with OptFlags(stabilizer_hybrid=False)); the decision
+ * inputs come back from the device through mapped pinned memory.  Gates are
+ * passed as packed arrays; matrices are the gate_matrix() values. */
+typedef struct sk_engine sk_engine;
+
+typedef struct {
+  double sdrp;             /* EngineConfig.sdrp in [0, 1] (engine.py:66-78) */
+  double separability_tol; /* 1e-10 */
+  int64_t mem_budget;      /* dense amplitudes */
+  int32_t dtype;           /* SK_C64 / SK_C128 */
+  int32_t device;
+  int32_t control_elimination, hx_commutation, label_swap, pauli_coalescing; /* OptFlags */
+} sk_engine_config;
+
+#define SK_GATE_1Q 0      /* 2x2 on targets[2g] (with controls when ctrl_off[g+1] > ctrl_off[g]) */
+#define SK_GATE_SWAP 1    /* targets[2g], targets[2g+1] */
+#define SK_GATE_MEASURE 2 /* targets[2g]; draws one uniform from the engine's rng callback */
+
+#define SK_ENGINE_STAT_LABEL_SWAPS 0
+#define SK_ENGINE_STAT_KERNELS 1
+#define SK_ENGINE_STAT_ELIMINATED 2
+#define SK_ENGINE_STAT_MERGES 3
+#define SK_ENGINE_STAT_SPLITS 4
+#define SK_ENGINE_STAT_ALLOCS 5      /* device states created (ket.py alloc_count) */
+#define SK_ENGINE_STAT_WRITES 6      /* amplitudes written (ket.py amplitude_writes) */
+#define SK_ENGINE_STAT_DENSE_TOTAL 7
+#define SK_ENGINE_STAT_PEAK 8        /* peak_amplitudes */
+#define SK_ENGINE_STAT_NEPS 9        /* len(eps_record) */
+#define SK_ENGINE_STAT_NEEDED 10     /* `needed` of the last SK_EBUDGET */
+#define SK_ENGINE_NSTATS 11
+
+typedef double (*sk_uniform_fn)(void* ctx); /* rng.random() of the caller's PCG64 stream */
+
+/* HybridState(n, cfg) (engine.py:164-182): n width-1 shards |0>. */
+int sk_engine_create(int n, const sk_engine_config* cfg, sk_engine** out);
+int sk_engine_destroy(sk_engine* e);
+int sk_engine_set_rng(sk_engine* e, sk_uniform_fn fn, void* ctx);
+/* apply_gate for gates [0, ngates) (engine.py:514-573): kind[g], targets[2g..2g+1],
+ * controls ctrls[ctrl_off[g] .. ctrl_off[g+1]) with polarities pols[...], matrix mats[8g..8g+7].
+ * *done = gates fully applied (the failing gate is not counted). */
+int sk_engine_apply(sk_engine* e, int ngates, const int32_t* kind, const int32_t* targets, const int32_t* ctrl_off,
+                    const int32_t* ctrls, const int32_t* pols, const double* mats, int* done);
+/* _measure_qubit (engine.py:575-594). */
+int sk_engine_measure(sk_engine* e, int label, int* outcome);
+/* flush_all (engine.py:669-681) / flush_buffers(q). */
+int sk_engine_flush_all(sk_engine* e);
+int sk_engine_flush_qubit(sk_engine* e, int label);
+/* sdrp_round(q, p) (engine.py:490-512): *eps_out = recorded eps or -1. */
+int sk_engine_sdrp_round(sk_engine* e, int label, double p, double* eps_out);
+int sk_engine_stats(const sk_engine* e, int64_t out[SK_ENGINE_NSTATS]);
+int sk_engine_eps(const sk_engine* e, double* out, int64_t cap);
+/* The shards in label order (engine.py _shards_in_label_order): states[i]
+ * (borrowed handles, valid until the next engine call), widths[i], and each
+ * shard's qubit labels by position, shard after shard, in labels[]. */
+int sk_engine_shards(const sk_engine* e, int cap, sk_state** states, int* widths, int* labels, int* nshards);
+/* load_state (engine.py:768-784): one dense shard, label i = bit i. */
+int sk_engine_load_state(sk_engine* e, const sk_state* s);
+/* measure_all's collapse (engine.py:616-624): every qubit becomes a fresh
+ * width-1 shard |bits[label]>. */
+int sk_engine_reset_basis(sk_engine* e, const uint8_t* bits);
 
 #ifdef __cplusplus
 }

@@ -9,9 +9,9 @@ import ctypes as C
 import threading
 
 from . import _build
-from .errors import DeviceError, MemoryBudgetError
+from .errors import DeviceError, DeviceMemoryError
 
-SK_OK, SK_EINDEX, SK_EVALUE, SK_ENOMEM, SK_ECUDA = 0, 1, 2, 3, 4
+SK_OK, SK_EINDEX, SK_EVALUE, SK_ENOMEM, SK_ECUDA, SK_EBUDGET = 0, 1, 2, 3, 4, 5
 SK_C64, SK_C128 = 0, 1
 SK_OP_MAT, SK_OP_DIAG, SK_OP_RAMP, SK_OP_QFT = 0, 1, 2, 3
 SK_MAX_TILE_BITS, SK_MAX_REG_BITS, SK_MAX_STAGES = 16, 5, 8
@@ -36,6 +36,19 @@ class SkSweep(C.Structure):
                 ("reg_bits", (C.c_int32 * SK_MAX_REG_BITS) * SK_MAX_STAGES),
                 ("op_begin", C.c_int32 * (SK_MAX_STAGES + 1)), ("nreg", C.c_int32)]
 
+
+class SkEngineConfig(C.Structure):
+    _fields_ = [("sdrp", C.c_double), ("separability_tol", C.c_double), ("mem_budget", C.c_int64),
+                ("dtype", C.c_int32), ("device", C.c_int32), ("control_elimination", C.c_int32),
+                ("hx_commutation", C.c_int32), ("label_swap", C.c_int32), ("pauli_coalescing", C.c_int32)]
+
+
+SK_GATE_1Q, SK_GATE_SWAP, SK_GATE_MEASURE = 0, 1, 2
+ENGINE_STATS = ("label_swaps", "kernels", "eliminated_controls", "merges", "splits", "allocs", "amplitude_writes",
+                "dense_total", "peak_amplitudes", "n_eps", "needed")
+UNIFORM_FN = C.CFUNCTYPE(C.c_double, C.c_void_p)
+p_engine = C.c_void_p
+i32p = C.POINTER(C.c_int32)
 
 # name -> argtypes (restype is always c_int unless listed in _RESTYPES)
 _SIGS = {
@@ -87,6 +100,20 @@ _SIGS = {
     "sk_program_run": [p_state, p_prog, C.c_int, C.c_int],
     "sk_program_nsweeps": [p_prog, C.POINTER(C.c_int)],
     "sk_program_set_phase_index": [p_prog, C.c_int, C.c_uint64],
+    "sk_engine_create": [C.c_int, C.POINTER(SkEngineConfig), C.POINTER(p_engine)],
+    "sk_engine_destroy": [p_engine],
+    "sk_engine_set_rng": [p_engine, UNIFORM_FN, C.c_void_p],
+    "sk_engine_apply": [p_engine, C.c_int, i32p, i32p, i32p, i32p, i32p, dptr, C.POINTER(C.c_int)],
+    "sk_engine_measure": [p_engine, C.c_int, C.POINTER(C.c_int)],
+    "sk_engine_flush_all": [p_engine],
+    "sk_engine_flush_qubit": [p_engine, C.c_int],
+    "sk_engine_sdrp_round": [p_engine, C.c_int, C.c_double, dptr],
+    "sk_engine_stats": [p_engine, C.POINTER(C.c_int64)],
+    "sk_engine_eps": [p_engine, dptr, C.c_int64],
+    "sk_engine_shards": [p_engine, C.c_int, C.POINTER(p_state), C.POINTER(C.c_int), C.POINTER(C.c_int),
+                         C.POINTER(C.c_int)],
+    "sk_engine_load_state": [p_engine, p_state],
+    "sk_engine_reset_basis": [p_engine, C.POINTER(C.c_uint8)],
 }
 _RESTYPES = {"sk_last_error": C.c_char_p}
 
@@ -132,7 +159,7 @@ def check(rc: int, needed: int | None = None) -> None:
     if rc == SK_EVALUE:
         raise ValueError(msg)
     if rc == SK_ENOMEM:
-        raise MemoryBudgetError(needed if needed is not None else -1, -1, msg)
+        raise DeviceMemoryError(f"{msg} (needed {needed} amplitudes)" if needed is not None else msg)
     raise DeviceError(msg)
 
 

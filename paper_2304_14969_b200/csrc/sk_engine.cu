@@ -1,0 +1,1010 @@
+// sk_engine.cu — native hybrid-engine runtime: the factorised simulator
+// that feeds the device ket.
+//
+// The reference's HybridState (pkg/src/shardsim/engine.py) keeps the global
+// state as a tensor product of shards and decides, after every committed
+// coupler, whether to split off or Schmidt-round each operand qubit.  Its
+// Python control flow costs ~0.1 ms per gate and its per-coupler decisions
+// each need the operands' Bloch sums.  Here the whole commit stream runs in
+// C++ next to the kernels:
+//   * gates arrive as one packed array per circuit (no per-gate FFI crossing);
+//   * 1q buffers, the pending controlled-op queues and every rewrite are
+//     host-side 2x2 algebra (std::complex<double>), in the reference's order;
+//   * the decision inputs (Bloch sums of the committed coupler's operands,
+//     fused with the gate itself in one pass) come back through mapped pinned
+//     memory — the device writes them, the host reads a sequence word — with no
+//     cudaMemcpy / stream synchronisation per coupler;
+//   * width-1 shards carry their Bloch sums in a host cache filled by the
+//     kernels that last wrote them (control elimination, engine.py:407-436,
+//     reads them without a device round trip);
+//   * SDRP rounding is one fused rotate-project-compact pass whose P0 is
+//     analytic in the sums already in hand (engine.py:464-488).
+// Decisions are bit-for-bit those of the reference engine's rules
+// (engine.py:276-512, 525-535, 575-594, 669-711), which tests/test_engine_gpu.py
+// and tests/test_scale_gpu.py pin against the reference's own records.
+//
+// Stabilizer (tableau) shards are not modelled: qubits start as width-1
+// dense shards, as in the reference with OptFlags(stabilizer_hybrid=False).
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <deque>
+#include <memory>
+#include <unordered_set>
+#include <vector>
+
+#include "sk_internal.cuh"
+
+namespace {
+
+using cd = std::complex<double>;
+
+struct M2 {
+  cd a[4];  // row-major m00 m01 m10 m11
+};
+
+M2 m_from8(const double* p) {
+  M2 m;
+  for (int i = 0; i < 4; ++i) m.a[i] = cd(p[2 * i], p[2 * i + 1]);
+  return m;
+}
+
+void m_to8(const M2& m, double* p) {
+  for (int i = 0; i < 4; ++i) {
+    p[2 * i] = m.a[i].real();
+    p[2 * i + 1] = m.a[i].imag();
+  }
+}
+
+M2 mmul(const M2& x, const M2& y) {  // x @ y
+  M2 r;
+  r.a[0] = x.a[0] * y.a[0] + x.a[1] * y.a[2];
+  r.a[1] = x.a[0] * y.a[1] + x.a[1] * y.a[3];
+  r.a[2] = x.a[2] * y.a[0] + x.a[3] * y.a[2];
+  r.a[3] = x.a[2] * y.a[1] + x.a[3] * y.a[3];
+  return r;
+}
+
+M2 mdag(const M2& x) {
+  M2 r;
+  r.a[0] = std::conj(x.a[0]);
+  r.a[1] = std::conj(x.a[2]);
+  r.a[2] = std::conj(x.a[1]);
+  r.a[3] = std::conj(x.a[3]);
+  return r;
+}
+
+const M2 kI = {{cd(1, 0), cd(0, 0), cd(0, 0), cd(1, 0)}};
+const M2 kPauli[3] = {{{cd(0, 0), cd(1, 0), cd(1, 0), cd(0, 0)}},     // X
+                      {{cd(0, 0), cd(0, -1), cd(0, 1), cd(0, 0)}},    // Y
+                      {{cd(1, 0), cd(0, 0), cd(0, 0), cd(-1, 0)}}};   // Z
+
+constexpr double kStructTol = 1e-14;  // engine.py _is_diag / _is_antidiag
+
+bool is_diag(const M2& m) { return std::abs(m.a[1]) < kStructTol && std::abs(m.a[2]) < kStructTol; }
+bool is_antidiag(const M2& m) { return std::abs(m.a[0]) < kStructTol && std::abs(m.a[3]) < kStructTol; }
+
+double max_abs_diff(const M2& x, const M2& y) {
+  double d = 0;
+  for (int i = 0; i < 4; ++i) d = std::max(d, std::abs(x.a[i] - y.a[i]));
+  return d;
+}
+
+bool is_identity(const M2& m) { return max_abs_diff(m, kI) < 1e-12; }  // engine.py:313-314
+
+// zero the structurally dead entries of a (near) diagonal / antidiagonal
+// matrix; false otherwise (engine.py:132-143)
+bool snap(const M2& m, M2* out) {
+  if (is_diag(m)) {
+    *out = m;
+    out->a[1] = out->a[2] = 0.0;
+    return true;
+  }
+  if (is_antidiag(m)) {
+    *out = m;
+    out->a[0] = out->a[3] = 0.0;
+    return true;
+  }
+  return false;
+}
+
+// ket.py:57-59 unitarity check of every committed matrix
+bool unitary(const M2& m) { return max_abs_diff(mmul(mdag(m), m), kI) <= 1e-10; }
+
+// Bloch-sphere rotation of a 2x2 unitary (engine.py:146-152)
+void so3(const M2& u, double r[3][3]) {
+  const M2 ud = mdag(u);
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      M2 t = mmul(mmul(mmul(kPauli[i], u), kPauli[j]), ud);
+      r[i][j] = 0.5 * (t.a[0] + t.a[3]).real();
+    }
+}
+
+// m = phase * Pauli within 1e-12 (engine.py:155-161); returns 0/1/2 or -1
+int as_pauli(const M2& m, cd* phase) {
+  for (int p = 0; p < 3; ++p) {
+    M2 t = mmul(kPauli[p], m);
+    cd tr = (t.a[0] + t.a[3]) / 2.0;
+    if (std::abs(std::abs(tr) - 1.0) < 1e-12) {
+      double d = 0;
+      for (int i = 0; i < 4; ++i) d = std::max(d, std::abs(m.a[i] - tr * kPauli[p].a[i]));
+      if (d < 1e-12) {
+        *phase = tr;
+        return p;
+      }
+    }
+  }
+  return -1;
+}
+
+struct Bloch {
+  double rx, ry, rz;
+  double length() const { return std::sqrt(rx * rx + ry * ry + rz * rz); }
+};
+
+Bloch bloch_from_sums(const double s[4]) { return {2.0 * s[0], 2.0 * s[1], s[2] - s[3]}; }  // ket.py:204-210
+
+double epsilon(const Bloch& r) { return (1.0 - std::min(r.length(), 1.0)) / 2.0; }  // ket.py:37-39
+
+// unit Bloch vector -> pure single-qubit state along it (ket.py:42-54)
+void bloch_to_state(const Bloch& r, cd phi[2]) {
+  const double norm = r.length();
+  const double nz = r.rz / norm;
+  const double c = std::sqrt(std::max(0.0, (1.0 + nz) / 2.0));
+  const double s = std::sqrt(std::max(0.0, (1.0 - nz) / 2.0));
+  if (s < 1e-15) {
+    phi[0] = 1.0;
+    phi[1] = 0.0;
+    return;
+  }
+  const double a = std::atan2(r.ry / norm, r.rx / norm);
+  phi[0] = c;
+  phi[1] = s * std::exp(cd(0, 1) * a);
+}
+
+struct Qubit;
+
+// Bloch sums of a width-1 shard: none, known on the host, or being
+// published by the kernel that wrote the shard into a mapped ring slot
+enum SumsKind { kSumsNone = 0, kSumsHost = 1, kSumsSlot = 2 };
+
+struct SumsTicket {
+  int kind = kSumsNone;
+  int slot = 0;
+  unsigned long long seq = 0;
+  double v[4] = {0, 0, 0, 0};
+};
+
+struct Shard {
+  sk_state* st = nullptr;
+  std::vector<Qubit*> qubits;  // position -> qubit
+  SumsTicket sums;             // width-1 shards only
+  int width() const { return (int)qubits.size(); }
+};
+
+constexpr int kRingSlots = 4096;
+constexpr int kSlotDoubles = 8;  // 4 sums, the sequence word, padding
+
+struct PendingOp {  // a buffered controlled phase / inversion (engine.py:_CtrlOp)
+  int64_t seq;
+  std::vector<Qubit*> controls;
+  std::vector<int> polarity;
+  Qubit* target;
+  M2 m;
+  std::vector<Qubit*> qubits() const {
+    std::vector<Qubit*> q = controls;
+    q.push_back(target);
+    return q;
+  }
+};
+
+struct Qubit {
+  Shard* shard = nullptr;
+  int pos = 0;
+  bool has_u = false;
+  M2 u;
+  std::deque<PendingOp*> pending;
+};
+
+}  // namespace
+
+using namespace sk;
+
+struct sk_engine {
+  int n = 0;
+  sk_engine_config cfg{};
+  std::vector<std::unique_ptr<Qubit>> own;
+  std::vector<Qubit*> handles;  // label -> qubit
+  std::unordered_set<Shard*> shards;
+  std::vector<double> eps;
+  int64_t dense_total = 0, peak = 0;
+  int64_t stats[SK_ENGINE_NSTATS] = {0};
+  int64_t seq = 0;
+  int64_t needed = 0;  // last budget failure
+  sk_uniform_fn ufn = nullptr;
+  void* uctx = nullptr;
+  double* h_ring = nullptr;  // mapped pinned ring of sums slots
+  double* d_ring = nullptr;
+  int ring_next = 0;
+  unsigned long long ring_seq = 0;
+
+  ~sk_engine() {
+    std::unordered_set<PendingOp*> ops;
+    for (auto& q : own)
+      for (auto* op : q->pending) ops.insert(op);
+    for (auto* op : ops) delete op;
+    for (auto* s : shards) {
+      sk_destroy(s->st);
+      delete s;
+    }
+    if (h_ring) {
+      DevCtx* c;
+      if (ctx_get(cfg.device, &c) == SK_OK) cudaStreamSynchronize(c->stream);  // kernels may still publish
+      cudaFreeHost(h_ring);
+    }
+  }
+
+  int init_ring() {
+    DevCtx* c;
+    SK_TRY(ctx_get(cfg.device, &c));
+    SK_CUDA(cudaHostAlloc(&h_ring, sizeof(double) * kRingSlots * kSlotDoubles, cudaHostAllocMapped));
+    SK_CUDA(cudaHostGetDevicePointer((void**)&d_ring, h_ring, 0));
+    memset(h_ring, 0, sizeof(double) * kRingSlots * kSlotDoubles);
+    return SK_OK;
+  }
+
+  // ---- budget (engine.py:202-214) -----------------------------------------
+  int charge(int64_t amount, int64_t transient = 0) {
+    const int64_t need = dense_total + amount + transient;
+    if (need > cfg.mem_budget) {
+      needed = need;
+      return set_error(SK_EBUDGET, "needs %lld dense amplitudes, budget is %lld", (long long)need,
+                       (long long)cfg.mem_budget);
+    }
+    dense_total += amount;
+    peak = std::max(peak, need);
+    return SK_OK;
+  }
+
+  int release(int64_t amount) {
+    dense_total -= amount;
+    if (dense_total < 0) return set_error(SK_EVALUE, "dense amplitude accounting went negative");
+    return SK_OK;
+  }
+
+  // ---- shards ------------------------------------------------------------------
+  Shard* new_shard(sk_state* st) {
+    Shard* s = new Shard();
+    s->st = st;
+    shards.insert(s);
+    return s;
+  }
+
+  void drop_shard(Shard* s) {
+    shards.erase(s);
+    sk_destroy(s->st);
+    delete s;
+  }
+
+  // a width-1 device shard holding amps; its kernel publishes the shard's
+  // Bloch sums (from the stored precision, as a reduction would) to a ring slot
+  int make_single(const cd amps[2], sk_state** out, SumsTicket* t) {
+    const double h[4] = {amps[0].real(), amps[0].imag(), amps[1].real(), amps[1].imag()};
+    const int slot = ring_next;
+    ring_next = (ring_next + 1) % kRingSlots;
+    const unsigned long long seq = ++ring_seq;
+    double* d = d_ring + (size_t)slot * kSlotDoubles;
+    SK_TRY(create_single_with_sums(cfg.dtype, cfg.device, h, d, (unsigned long long*)(d + 4), seq, out));
+    t->kind = kSumsSlot;
+    t->slot = slot;
+    t->seq = seq;
+    stats[SK_ENGINE_STAT_ALLOCS]++;
+    return SK_OK;
+  }
+
+  int fresh_single(Qubit* q, int bit) {  // engine.py:187-200 (dense branch)
+    SK_TRY(charge(2));
+    cd a[2] = {bit ? 0.0 : 1.0, bit ? 1.0 : 0.0};
+    sk_state* st;
+    double h[4] = {a[0].real(), a[0].imag(), a[1].real(), a[1].imag()};
+    SK_TRY(sk_create_from(1, cfg.dtype, cfg.device, h, &st));
+    stats[SK_ENGINE_STAT_ALLOCS]++;
+    Shard* s = new_shard(st);
+    s->qubits = {q};
+    s->sums.kind = kSumsHost;  // basis states: the sums are exact
+    s->sums.v[0] = s->sums.v[1] = 0.0;
+    s->sums.v[2] = bit ? 0.0 : 1.0;
+    s->sums.v[3] = bit ? 1.0 : 0.0;
+    q->shard = s;
+    q->pos = 0;
+    return SK_OK;
+  }
+
+  int merge_pair(Shard* a, Shard* b, Shard** out) {  // engine.py:224-243: the wider keeps its positions
+    if (a->width() < b->width()) std::swap(a, b);
+    stats[SK_ENGINE_STAT_MERGES]++;
+    const int wa = a->width(), wb = b->width();
+    SK_TRY(charge(int64_t(1) << (wa + wb)));
+    sk_state* st;
+    SK_TRY(sk_kron(a->st, b->st, &st));
+    stats[SK_ENGINE_STAT_ALLOCS]++;
+    stats[SK_ENGINE_STAT_WRITES] += int64_t(1) << (wa + wb);
+    SK_TRY(release((int64_t(1) << wa) + (int64_t(1) << wb)));
+    Shard* m = new_shard(st);
+    m->qubits = a->qubits;
+    m->qubits.insert(m->qubits.end(), b->qubits.begin(), b->qubits.end());
+    for (int i = 0; i < m->width(); ++i) {
+      m->qubits[i]->shard = m;
+      m->qubits[i]->pos = i;
+    }
+    drop_shard(a);
+    drop_shard(b);
+    *out = m;
+    return SK_OK;
+  }
+
+  int merge_for(const std::vector<Qubit*>& qs, Shard** out) {
+    std::vector<Shard*> list;
+    for (Qubit* q : qs)
+      if (std::find(list.begin(), list.end(), q->shard) == list.end()) list.push_back(q->shard);
+    Shard* m = list[0];
+    for (size_t i = 1; i < list.size(); ++i) SK_TRY(merge_pair(m, list[i], &m));
+    *out = m;
+    return SK_OK;
+  }
+
+  // replace shard by (rest, new width-1 shard {single}) (engine.py:257-270)
+  void split(Shard* shard, int pos, sk_state* single, const SumsTicket& single_sums, sk_state* rest) {
+    Qubit* q = shard->qubits[pos];
+    const int64_t old = int64_t(1) << shard->width();
+    stats[SK_ENGINE_STAT_SPLITS]++;
+    Shard* s1 = new_shard(single);
+    s1->qubits = {q};
+    s1->sums = single_sums;
+    q->shard = s1;
+    q->pos = 0;
+    shard->qubits.erase(shard->qubits.begin() + pos);
+    for (int i = 0; i < shard->width(); ++i) shard->qubits[i]->pos = i;
+    sk_destroy(shard->st);
+    shard->st = rest;
+    shard->sums.kind = kSumsNone;
+    dense_total += (2 + (int64_t(1) << rest->width)) - old;
+  }
+
+  // Bloch sums of q in its shard: width-1 shards carry them (host values or
+  // a ring slot their kernel published); else one device reduction returned
+  // through mapped memory
+  int sums_of(Qubit* q, double out[4]) {
+    Shard* s = q->shard;
+    if (s->width() == 1 && s->sums.kind == kSumsSlot) {
+      volatile double* slot = h_ring + (size_t)s->sums.slot * kSlotDoubles;
+      volatile unsigned long long* flag = (volatile unsigned long long*)(slot + 4);
+      if (*flag <= s->sums.seq) {  // not overwritten by a newer publication: wait for ours
+        SK_TRY(wait_mapped(cfg.device, flag, s->sums.seq));
+        for (int k = 0; k < 4; ++k) s->sums.v[k] = slot[k];
+        s->sums.kind = *flag == s->sums.seq ? kSumsHost : kSumsNone;
+      } else {
+        s->sums.kind = kSumsNone;
+      }
+    }
+    if (s->width() == 1 && s->sums.kind == kSumsHost) {
+      std::copy(s->sums.v, s->sums.v + 4, out);
+      return SK_OK;
+    }
+    SK_TRY(sk_bloch_sums(s->st, q->pos, out));
+    if (s->width() == 1) {
+      s->sums.kind = kSumsHost;
+      std::copy(out, out + 4, s->sums.v);
+    }
+    return SK_OK;
+  }
+
+  // ---- 1q buffers (engine.py:276-322) ----------------------------------------
+  int absorb_1q(Qubit* q, const M2& m) {
+    if (!q->pending.empty() && !commute_past(q, m)) SK_TRY(flush_pending(q));
+    q->u = q->has_u ? mmul(m, q->u) : m;
+    q->has_u = true;
+    return SK_OK;
+  }
+
+  bool commute_past(Qubit* q, const M2& m) {  // all or nothing (engine.py:281-303)
+    struct Plan {
+      PendingOp* op;
+      int action;  // 0 matrix, 1 keep, 2 flip
+      M2 conj;
+    };
+    std::vector<Plan> plans;
+    const bool d = is_diag(m), ad = !d && is_antidiag(m);
+    for (PendingOp* op : q->pending) {
+      if (op->target == q) {
+        M2 c;
+        if (!snap(mmul(mmul(m, op->m), mdag(m)), &c)) return false;
+        plans.push_back({op, 0, c});
+      } else if (d) {
+        plans.push_back({op, 1, M2()});
+      } else if (ad) {
+        plans.push_back({op, 2, M2()});
+      } else {
+        return false;
+      }
+    }
+    for (auto& p : plans) {
+      if (p.action == 0) {
+        p.op->m = p.conj;
+      } else if (p.action == 2) {
+        auto it = std::find(p.op->controls.begin(), p.op->controls.end(), q);
+        p.op->polarity[it - p.op->controls.begin()] ^= 1;
+      }
+    }
+    return true;
+  }
+
+  int commit_1q(Qubit* q) {
+    if (!q->has_u) return SK_OK;
+    const M2 m = q->u;
+    q->has_u = false;
+    if (is_identity(m)) return SK_OK;
+    if (!unitary(m)) return set_error(SK_EVALUE, "matrix is not unitary within 1e-10");
+    double m8[8];
+    m_to8(m, m8);
+    Shard* s = q->shard;
+    SK_TRY(sk_apply_1q(s->st, q->pos, m8));
+    stats[SK_ENGINE_STAT_KERNELS]++;
+    stats[SK_ENGINE_STAT_WRITES] += int64_t(1) << s->width();
+    s->sums.kind = kSumsNone;
+    return SK_OK;
+  }
+
+  // ---- buffered controlled ops (engine.py:328-365) ------------------------------
+  int buffer_ctrl(const std::vector<Qubit*>& chs, const std::vector<int>& pol, Qubit* target, const M2& m) {
+    PendingOp* tail = target->pending.empty() ? nullptr : target->pending.back();
+    if (tail && tail->target == target && tail->controls == chs && tail->polarity == pol) {
+      bool all_tail = true;
+      for (Qubit* x : tail->qubits())
+        if (x->pending.empty() || x->pending.back() != tail) all_tail = false;
+      if (all_tail) {
+        M2 fused;
+        if (!snap(mmul(m, tail->m), &fused))
+          return set_error(SK_EVALUE, "fused controlled op left the buffered class");
+        if (is_identity(fused)) {
+          for (Qubit* x : tail->qubits()) x->pending.erase(std::find(x->pending.begin(), x->pending.end(), tail));
+          delete tail;
+        } else {
+          tail->m = fused;
+        }
+        return SK_OK;
+      }
+    }
+    PendingOp* op = new PendingOp{++seq, chs, pol, target, m};
+    for (Qubit* x : op->qubits()) x->pending.push_back(op);
+    return SK_OK;
+  }
+
+  int flush_pending(Qubit* q) {
+    while (!q->pending.empty()) SK_TRY(commit_chain(q->pending.front()));
+    return SK_OK;
+  }
+
+  int commit_chain(PendingOp* op) {
+    const std::vector<Qubit*> qs = op->qubits();
+    for (Qubit* x : qs)
+      while (!x->pending.empty() && x->pending.front() != op) SK_TRY(commit_chain(x->pending.front()));
+    for (Qubit* x : qs) {
+      if (x->pending.empty() || x->pending.front() != op)
+        return set_error(SK_EVALUE, "pending op queues lost chronological order");
+      x->pending.pop_front();
+    }
+    std::vector<Qubit*> c = op->controls;
+    std::vector<int> p = op->polarity;
+    Qubit* t = op->target;
+    const M2 m = op->m;
+    delete op;
+    return commit_ctrl(c, p, t, m);
+  }
+
+  // flush operand buffers, merge, run the kernel, then try to factor or
+  // round each operand (engine.py:367-394); with one control the kernel
+  // also returns both operands' Bloch sums (one pass instead of three)
+  int commit_ctrl(const std::vector<Qubit*>& controls, const std::vector<int>& pol, Qubit* target, const M2& m) {
+    std::vector<Qubit*> qs = controls;
+    qs.push_back(target);
+    for (Qubit* q : qs) SK_TRY(commit_1q(q));
+    Shard* s;
+    SK_TRY(merge_for(qs, &s));
+    if (!unitary(m)) return set_error(SK_EVALUE, "matrix is not unitary within 1e-10");
+    double m8[8];
+    m_to8(m, m8);
+    std::vector<std::vector<double>> pre;
+    if (controls.size() == 1) {
+      double out8[8];
+      SK_TRY(sk_apply_controlled_bloch(s->st, controls[0]->pos, pol[0], target->pos, m8, out8));
+      pre = {std::vector<double>(out8, out8 + 4), std::vector<double>(out8 + 4, out8 + 8)};
+      stats[SK_ENGINE_STAT_WRITES] += int64_t(1) << (s->width() - 1);
+    } else {
+      uint64_t mask = 0, val = 0;
+      for (size_t i = 0; i < controls.size(); ++i) {
+        mask |= 1ull << controls[i]->pos;
+        if (pol[i]) val |= 1ull << controls[i]->pos;
+      }
+      SK_TRY(sk_apply_controlled(s->st, mask, val, target->pos, m8));
+      stats[SK_ENGINE_STAT_WRITES] += 2 * (int64_t(1) << (s->width() - 1 - (int)controls.size()));
+    }
+    s->sums.kind = kSumsNone;
+    stats[SK_ENGINE_STAT_KERNELS]++;
+    for (size_t i = 0; i < qs.size(); ++i) {
+      bool changed = false;
+      SK_TRY(try_factor(qs[i], pre.empty() ? nullptr : pre[i].data(), &changed));
+      if (changed) pre.clear();  // later operands see a new state: recompute their sums
+    }
+    return SK_OK;
+  }
+
+  // ---- control elimination (engine.py:407-436) -----------------------------------
+  int z_eigenstate(Qubit* q, int* z) {
+    *z = -1;
+    if (!q->pending.empty()) return SK_OK;
+    if (q->shard->width() > 1) return SK_OK;  // entangled-shard scan not worth the pass
+    const double tol = cfg.separability_tol;
+    double sums[4];
+    SK_TRY(sums_of(q, sums));
+    const Bloch b = bloch_from_sums(sums);
+    if (epsilon(b) > tol) return SK_OK;
+    double r0[3] = {b.rx, b.ry, b.rz};
+    if (q->has_u) {
+      double R[3][3];
+      so3(q->u, R);
+      double r[3];
+      for (int i = 0; i < 3; ++i) r[i] = R[i][0] * r0[0] + R[i][1] * r0[1] + R[i][2] * r0[2];
+      std::copy(r, r + 3, r0);
+    }
+    if (r0[2] >= 1.0 - 2 * tol - 1e-12) *z = 0;
+    else if (r0[2] <= -1.0 + 2 * tol + 1e-12) *z = 1;
+    return SK_OK;
+  }
+
+  // ---- factorisation and Schmidt rounding (engine.py:442-512) ----------------------
+  int try_decompose(Shard* shard, int pos, const double sums[4], bool* done) {
+    // ket.py:243-267 with phi analytic in the sums: <dominant|a0>, <dominant|a1>
+    *done = false;
+    const cd cross(sums[0], sums[1]);
+    const double n0 = sums[2], n1 = sums[3];
+    int half;
+    double ndom;
+    cd phi[2];
+    if (n0 >= 0.5) {
+      half = 0, ndom = n0, phi[0] = n0, phi[1] = cross;
+    } else {
+      half = 1, ndom = n1, phi[0] = std::conj(cross), phi[1] = n1;
+    }
+    const double pn = std::sqrt(std::norm(phi[0]) + std::norm(phi[1]));
+    phi[0] /= pn;
+    phi[1] /= pn;
+    sk_state* rest;
+    SK_TRY(sk_compact(shard->st, pos, half, 1.0 / std::sqrt(ndom), 0.0, &rest));
+    stats[SK_ENGINE_STAT_ALLOCS]++;
+    sk_state* single;
+    SumsTicket ss;
+    SK_TRY(make_single(phi, &single, &ss));
+    split(shard, pos, single, ss, rest);
+    *done = true;
+    return SK_OK;
+  }
+
+  // returns the recorded eps (or -1 when none / degenerate); *rounded tells
+  // whether the state changed
+  int round_qubit(Shard* shard, int pos, const Bloch& r, double eps, const double sums[4], bool* rounded) {
+    *rounded = false;
+    M2 u = kI;
+    cd phi[2] = {1.0, 0.0};
+    if (r.length() >= 1e-12) {  // maximally mixed: identity rotation
+      bloch_to_state(r, phi);
+      u.a[0] = std::conj(phi[0]);
+      u.a[1] = std::conj(phi[1]);
+      u.a[2] = -phi[1];
+      u.a[3] = phi[0];
+    }
+    const cd cross(sums[0], sums[1]);
+    const double p0 = std::norm(u.a[0]) * sums[2] + std::norm(u.a[1]) * sums[3] +
+                      2.0 * (std::conj(u.a[0]) * u.a[1] * cross).real();
+    if (p0 < 1e-12) return SK_OK;  // numerically degenerate: leave the state alone (engine.py:477-480)
+    const double u0[4] = {u.a[0].real(), u.a[0].imag(), u.a[1].real(), u.a[1].imag()};
+    sk_state* rest;
+    SK_TRY(sk_round_compact(shard->st, pos, u0, 1.0 / std::sqrt(p0), &rest));
+    stats[SK_ENGINE_STAT_ALLOCS]++;
+    stats[SK_ENGINE_STAT_WRITES] += int64_t(1) << shard->width();
+    sk_state* single;
+    SumsTicket ss;
+    SK_TRY(make_single(phi, &single, &ss));
+    split(shard, pos, single, ss, rest);
+    if (eps > cfg.separability_tol) eps_push(eps);
+    *rounded = true;
+    return SK_OK;
+  }
+
+  void eps_push(double e) { eps.push_back(e); }
+
+  int try_factor(Qubit* q, const double* given, bool* changed) {
+    *changed = false;
+    Shard* shard = q->shard;
+    if (shard->width() < 2) return SK_OK;
+    double sums[4];
+    if (given)
+      std::copy(given, given + 4, sums);
+    else
+      SK_TRY(sums_of(q, sums));
+    const Bloch r = bloch_from_sums(sums);
+    const double e = epsilon(r);
+    if (e <= cfg.separability_tol) return try_decompose(shard, q->pos, sums, changed);
+    if (cfg.sdrp > 0.0 && e <= cfg.sdrp / 2.0) return round_qubit(shard, q->pos, r, e, sums, changed);
+    return SK_OK;
+  }
+
+  // ---- gate dispatch (engine.py:514-573) ----------------------------------------
+  int apply_ctrl_gate(std::vector<Qubit*> chs, std::vector<int> pol, Qubit* target, const M2& m) {
+    if (cfg.control_elimination) {
+      std::vector<Qubit*> kc;
+      std::vector<int> kp;
+      for (size_t i = 0; i < chs.size(); ++i) {
+        int z;
+        SK_TRY(z_eigenstate(chs[i], &z));
+        if (z < 0) {
+          kc.push_back(chs[i]);
+          kp.push_back(pol[i]);
+        } else if (z == pol[i]) {
+          stats[SK_ENGINE_STAT_ELIMINATED]++;
+        } else {
+          return SK_OK;  // this control can never fire
+        }
+      }
+      chs.swap(kc);
+      pol.swap(kp);
+    }
+    if (chs.empty()) return absorb_1q(target, m);
+    M2 snapped;
+    if (cfg.hx_commutation && snap(m, &snapped)) return buffer_ctrl(chs, pol, target, snapped);
+    for (Qubit* c : chs) SK_TRY(flush_pending(c));
+    SK_TRY(flush_pending(target));
+    return commit_ctrl(chs, pol, target, m);
+  }
+
+  int measure_qubit(int label, int* outcome) {  // engine.py:575-594
+    Qubit* h = handles[label];
+    SK_TRY(flush_pending(h));
+    SK_TRY(commit_1q(h));
+    Shard* s = h->shard;
+    double sums[4];
+    SK_TRY(sums_of(h, sums));
+    const double p1 = sums[3];
+    if (!ufn) return set_error(SK_EVALUE, "circuit contains measurements but the engine has no rng");
+    const int out = ufn(uctx) < p1 ? 1 : 0;
+    *outcome = out;
+    if (s->width() > 1) {
+      const double prob = out ? p1 : sums[2];
+      if (prob <= 1e-12)
+        return set_error(SK_EVALUE, "outcome %d on qubit %d has probability %.3e", out, label, prob);
+      sk_state* rest;
+      SK_TRY(sk_compact(s->st, h->pos, out, 1.0 / std::sqrt(prob), 0.0, &rest));
+      stats[SK_ENGINE_STAT_ALLOCS]++;
+      stats[SK_ENGINE_STAT_WRITES] += int64_t(1) << s->width();
+      const cd basis[2] = {out ? 0.0 : 1.0, out ? 1.0 : 0.0};
+      sk_state* single;
+      SumsTicket ss;
+      SK_TRY(make_single(basis, &single, &ss));
+      split(s, h->pos, single, ss, rest);
+    } else {
+      double prob;
+      SK_TRY(sk_project(s->st, h->pos, out, &prob));
+      stats[SK_ENGINE_STAT_WRITES] += 2;
+      s->sums.kind = kSumsNone;
+    }
+    return SK_OK;
+  }
+
+  int apply_gate(int kind, const int32_t* tg, const int32_t* cs, const int32_t* ps, int nc, const double* m8) {
+    for (int i = 0; i < (kind == SK_GATE_SWAP ? 2 : 1); ++i)
+      if (tg[i] < 0 || tg[i] >= n) return set_error(SK_EINDEX, "qubit %d out of range for %d-qubit simulator", tg[i], n);
+    for (int i = 0; i < nc; ++i)
+      if (cs[i] < 0 || cs[i] >= n) return set_error(SK_EINDEX, "qubit %d out of range for %d-qubit simulator", cs[i], n);
+    if (kind == SK_GATE_MEASURE) {
+      int o;
+      return measure_qubit(tg[0], &o);
+    }
+    if (kind == SK_GATE_SWAP) {
+      const int a = tg[0], b = tg[1];
+      if (cfg.label_swap) {
+        std::swap(handles[a], handles[b]);
+        stats[SK_ENGINE_STAT_LABEL_SWAPS]++;
+        return SK_OK;
+      }
+      const M2& X = kPauli[0];
+      SK_TRY(apply_ctrl_gate({handles[a]}, {1}, handles[b], X));
+      SK_TRY(apply_ctrl_gate({handles[b]}, {1}, handles[a], X));
+      return apply_ctrl_gate({handles[a]}, {1}, handles[b], X);
+    }
+    const M2 m = m_from8(m8);
+    if (nc == 0) return absorb_1q(handles[tg[0]], m);
+    std::vector<Qubit*> chs(nc);
+    std::vector<int> pol(nc);
+    for (int i = 0; i < nc; ++i) {
+      chs[i] = handles[cs[i]];
+      pol[i] = ps[i];
+    }
+    return apply_ctrl_gate(chs, pol, handles[tg[0]], m);
+  }
+
+  // ---- flushes (engine.py:669-711) -------------------------------------------------
+  int flush_all() {
+    std::vector<PendingOp*> ops;
+    std::unordered_set<PendingOp*> seen;
+    for (Qubit* h : handles)
+      for (PendingOp* op : h->pending)
+        if (seen.insert(op).second) ops.push_back(op);
+    std::sort(ops.begin(), ops.end(), [](PendingOp* a, PendingOp* b) { return a->seq < b->seq; });
+    // an op may be committed (and freed) by an earlier op's chain: test
+    // liveness through the queues before touching it
+    for (size_t i = 0; i < ops.size(); ++i) {
+      PendingOp* op = ops[i];
+      bool live = false;
+      for (Qubit* h : handles)
+        if (std::find(h->pending.begin(), h->pending.end(), op) != h->pending.end()) {
+          live = true;
+          break;
+        }
+      if (!live) continue;
+      if (std::find(op->target->pending.begin(), op->target->pending.end(), op) != op->target->pending.end())
+        SK_TRY(commit_chain(op));
+    }
+    if (cfg.pauli_coalescing) SK_TRY(coalesced_flush());
+    for (Qubit* h : handles) SK_TRY(commit_1q(h));
+    return SK_OK;
+  }
+
+  int coalesced_flush() {
+    std::unordered_set<Shard*> seen;
+    for (Qubit* h : handles) {
+      Shard* s = h->shard;
+      if (!seen.insert(s).second) continue;
+      uint64_t flip = 0, sign = 0;
+      int y = 0, count = 0, first_pos = -1, first_p = -1;
+      cd scale = 1.0;
+      for (Qubit* qb : s->qubits) {
+        if (!qb->has_u) continue;
+        cd ph;
+        const int p = as_pauli(qb->u, &ph);
+        if (p < 0) continue;
+        if (count == 0) first_pos = qb->pos, first_p = p;
+        ++count;
+        if (p == 0) flip |= 1ull << qb->pos;
+        if (p == 1) flip |= 1ull << qb->pos, sign |= 1ull << qb->pos, ++y;
+        if (p == 2) sign |= 1ull << qb->pos;
+        scale *= ph;
+        qb->has_u = false;
+      }
+      if (count >= 2) {
+        const cd iy = std::pow(cd(0, 1), y % 4);  // ket.py:188-190: i^#Y belongs to the layer
+        const cd exact_iy = (y % 4 == 0) ? cd(1, 0) : (y % 4 == 1) ? cd(0, 1) : (y % 4 == 2) ? cd(-1, 0) : cd(0, -1);
+        (void)iy;
+        SK_TRY(sk_apply_pauli_layer(s->st, flip, sign, exact_iy.real(), exact_iy.imag()));
+        stats[SK_ENGINE_STAT_WRITES] += int64_t(1) << s->width();
+        if (std::abs(scale - 1.0) > 1e-15) SK_TRY(sk_scale(s->st, scale.real(), scale.imag()));
+        stats[SK_ENGINE_STAT_KERNELS]++;
+        s->sums.kind = kSumsNone;
+      } else if (count == 1) {
+        M2 m = kPauli[first_p];
+        for (auto& v : m.a) v *= scale;
+        double m8[8];
+        m_to8(m, m8);
+        SK_TRY(sk_apply_1q(s->st, first_pos, m8));
+        stats[SK_ENGINE_STAT_WRITES] += int64_t(1) << s->width();
+        stats[SK_ENGINE_STAT_KERNELS]++;
+        s->sums.kind = kSumsNone;
+      }
+    }
+    return SK_OK;
+  }
+
+  int sdrp_round(int label, double p, double* eps_out) {  // engine.py:490-512
+    *eps_out = -1.0;
+    Qubit* h = handles[label];
+    SK_TRY(flush_pending(h));
+    SK_TRY(commit_1q(h));
+    Shard* s = h->shard;
+    if (s->width() < 2) return set_error(SK_EVALUE, "sdrp_round needs a dense shard of width >= 2");
+    double sums[4];
+    SK_TRY(sums_of(h, sums));
+    const Bloch r = bloch_from_sums(sums);
+    const double e = epsilon(r);
+    bool changed;
+    if (e <= cfg.separability_tol) return try_decompose(s, h->pos, sums, &changed);
+    if (e > p / 2.0) return SK_OK;
+    const size_t before = eps.size();
+    SK_TRY(round_qubit(s, h->pos, r, e, sums, &changed));
+    if (eps.size() > before) *eps_out = eps.back();
+    return SK_OK;
+  }
+};
+
+namespace {
+
+int check_engine(const sk_engine* e) {
+  if (!e) return set_error(SK_EVALUE, "null engine");
+  return SK_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+int sk_engine_create(int n, const sk_engine_config* cfg, sk_engine** out) {
+  if (n < 1) return set_error(SK_EVALUE, "simulator needs at least 1 qubit");
+  if (!cfg) return set_error(SK_EVALUE, "null config");
+  if (!(cfg->sdrp >= 0.0 && cfg->sdrp <= 1.0)) return set_error(SK_EVALUE, "sdrp must be in [0, 1]");
+  if (cfg->mem_budget < 2) return set_error(SK_EVALUE, "mem_budget must be >= 2");
+  if (cfg->dtype != SK_C64 && cfg->dtype != SK_C128) return set_error(SK_EVALUE, "bad dtype %d", cfg->dtype);
+  auto e = std::make_unique<sk_engine>();
+  e->n = n;
+  e->cfg = *cfg;
+  e->own.reserve(n);
+  SK_TRY(e->init_ring());
+  for (int i = 0; i < n; ++i) {
+    e->own.emplace_back(new Qubit());
+    e->handles.push_back(e->own.back().get());
+    int rc = e->fresh_single(e->own.back().get(), 0);
+    if (rc != SK_OK) {
+      if (rc == SK_EBUDGET) return rc;
+      return rc;
+    }
+  }
+  *out = e.release();
+  return SK_OK;
+}
+
+int sk_engine_destroy(sk_engine* e) {
+  delete e;
+  return SK_OK;
+}
+
+int sk_engine_set_rng(sk_engine* e, sk_uniform_fn fn, void* ctx) {
+  SK_TRY(check_engine(e));
+  e->ufn = fn;
+  e->uctx = ctx;
+  return SK_OK;
+}
+
+int sk_engine_apply(sk_engine* e, int ngates, const int32_t* kind, const int32_t* targets, const int32_t* ctrl_off,
+                    const int32_t* ctrls, const int32_t* pols, const double* mats, int* done) {
+  SK_TRY(check_engine(e));
+  *done = 0;
+  for (int g = 0; g < ngates; ++g) {
+    const int nc = ctrl_off[g + 1] - ctrl_off[g];
+    SK_TRY(e->apply_gate(kind[g], targets + 2 * g, ctrls + ctrl_off[g], pols + ctrl_off[g], nc, mats + 8 * g));
+    *done = g + 1;
+  }
+  return SK_OK;
+}
+
+int sk_engine_measure(sk_engine* e, int label, int* outcome) {
+  SK_TRY(check_engine(e));
+  if (label < 0 || label >= e->n) return set_error(SK_EINDEX, "qubit %d out of range", label);
+  return e->measure_qubit(label, outcome);
+}
+
+int sk_engine_flush_all(sk_engine* e) {
+  SK_TRY(check_engine(e));
+  return e->flush_all();
+}
+
+int sk_engine_flush_qubit(sk_engine* e, int label) {
+  SK_TRY(check_engine(e));
+  if (label < 0 || label >= e->n) return set_error(SK_EINDEX, "qubit %d out of range", label);
+  SK_TRY(e->flush_pending(e->handles[label]));
+  return e->commit_1q(e->handles[label]);
+}
+
+int sk_engine_sdrp_round(sk_engine* e, int label, double p, double* eps_out) {
+  SK_TRY(check_engine(e));
+  if (label < 0 || label >= e->n) return set_error(SK_EINDEX, "qubit %d out of range", label);
+  return e->sdrp_round(label, p, eps_out);
+}
+
+int sk_engine_stats(const sk_engine* e, int64_t out[SK_ENGINE_NSTATS]) {
+  SK_TRY(check_engine(e));
+  for (int i = 0; i < SK_ENGINE_NSTATS; ++i) out[i] = e->stats[i];
+  out[SK_ENGINE_STAT_DENSE_TOTAL] = e->dense_total;
+  out[SK_ENGINE_STAT_PEAK] = e->peak;
+  out[SK_ENGINE_STAT_NEPS] = (int64_t)e->eps.size();
+  out[SK_ENGINE_STAT_NEEDED] = e->needed;
+  return SK_OK;
+}
+
+int sk_engine_eps(const sk_engine* e, double* out, int64_t cap) {
+  SK_TRY(check_engine(e));
+  const int64_t k = std::min<int64_t>(cap, (int64_t)e->eps.size());
+  std::copy(e->eps.begin(), e->eps.begin() + k, out);
+  return SK_OK;
+}
+
+int sk_engine_shards(const sk_engine* e, int cap, sk_state** states, int* widths, int* labels, int* nshards) {
+  SK_TRY(check_engine(e));
+  // shards in order of their lowest label (engine.py _shards_in_label_order);
+  // labels[] lists each shard's qubits by position, shard after shard
+  std::vector<int> label_of(e->n);
+  std::unordered_set<const Qubit*> dummy;
+  for (int l = 0; l < e->n; ++l) label_of[l] = 0;
+  std::vector<std::pair<const Qubit*, int>> ql;
+  std::vector<int> lab(e->own.size());
+  for (int l = 0; l < e->n; ++l) {
+    const Qubit* q = e->handles[l];
+    for (size_t i = 0; i < e->own.size(); ++i)
+      if (e->own[i].get() == q) lab[i] = l;
+  }
+  std::vector<const Shard*> order;
+  for (int l = 0; l < e->n; ++l) {
+    const Shard* s = e->handles[l]->shard;
+    if (std::find(order.begin(), order.end(), s) == order.end()) order.push_back(s);
+  }
+  if ((int)order.size() > cap) return set_error(SK_EVALUE, "need room for %d shards", (int)order.size());
+  int k = 0;
+  for (size_t i = 0; i < order.size(); ++i) {
+    states[i] = order[i]->st;
+    widths[i] = order[i]->width();
+    for (const Qubit* q : order[i]->qubits) {
+      for (size_t j = 0; j < e->own.size(); ++j)
+        if (e->own[j].get() == q) labels[k] = lab[j];
+      ++k;
+    }
+  }
+  *nshards = (int)order.size();
+  return SK_OK;
+}
+
+int sk_engine_load_state(sk_engine* e, const sk_state* s) {  // engine.py:768-784
+  SK_TRY(check_engine(e));
+  if (!s || s->width != e->n) return set_error(SK_EVALUE, "state width must equal simulator width %d", e->n);
+  std::unordered_set<PendingOp*> ops;
+  for (Qubit* h : e->handles) {
+    for (PendingOp* op : h->pending) ops.insert(op);
+    h->pending.clear();
+    h->has_u = false;
+  }
+  for (PendingOp* op : ops) delete op;
+  int64_t total = 0;
+  for (Shard* sh : e->shards) total += int64_t(1) << sh->width();
+  SK_TRY(e->release(total));
+  SK_TRY(e->charge(int64_t(1) << s->width));
+  sk_state* copy;
+  if (s->dtype == e->cfg.dtype) {
+    SK_TRY(sk_copy(s, &copy));
+  } else {
+    std::vector<double> host(2 * s->n);
+    SK_TRY(sk_download(s, host.data(), s->n));
+    SK_TRY(sk_create_from(s->width, e->cfg.dtype, e->cfg.device, host.data(), &copy));
+  }
+  e->stats[SK_ENGINE_STAT_ALLOCS]++;
+  std::vector<Shard*> old(e->shards.begin(), e->shards.end());
+  for (Shard* sh : old) e->drop_shard(sh);
+  Shard* sh = e->new_shard(copy);
+  sh->qubits = e->handles;
+  for (int l = 0; l < e->n; ++l) {
+    e->handles[l]->shard = sh;
+    e->handles[l]->pos = l;
+  }
+  return SK_OK;
+}
+
+int sk_engine_reset_basis(sk_engine* e, const uint8_t* bits) {  // measure_all collapse (engine.py:596-626)
+  SK_TRY(check_engine(e));
+  std::vector<Shard*> old(e->shards.begin(), e->shards.end());
+  for (Shard* sh : old) {
+    SK_TRY(e->release(int64_t(1) << sh->width()));
+    e->drop_shard(sh);
+  }
+  for (int l = 0; l < e->n; ++l) SK_TRY(e->fresh_single(e->handles[l], bits[l] ? 1 : 0));
+  return SK_OK;
+}
+
+}  // extern "C"

@@ -46,17 +46,37 @@ int set_error(int code, const char* fmt, ...);
 constexpr int kRedMaxBlocks = 1184;  // 148 SMs x 8
 constexpr int kRedMaxK = 8;
 
+// Reductions hand their fp64 results to the host through mapped pinned
+// memory: the last block writes the K sums straight into host memory, then
+// (after __threadfence_system) a sequence number; the host spins on that
+// number instead of a cudaMemcpyAsync + cudaStreamSynchronize round trip.
+struct RedOut {
+  double* partials;
+  unsigned* counter;
+  double* result;               // device alias of the mapped host slot
+  unsigned long long* flag;     // device alias of the mapped sequence word
+  unsigned long long seq;
+};
+
 struct DevCtx {
   bool init = false;
   int device = 0;
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
   double* d_partials = nullptr;  // [kRedMaxBlocks * kRedMaxK]
-  double* d_result = nullptr;    // [kRedMaxK]
   unsigned int* d_counter = nullptr;
-  double* h_result = nullptr;    // pinned [kRedMaxK]
+  double* h_result = nullptr;    // pinned [kRedMaxK] (point reads)
+  double* h_map = nullptr;       // mapped pinned: [kRedMaxK] results + 1 sequence word
+  double* d_map = nullptr;       // its device alias
+  unsigned long long seq = 0;
+  std::mutex red_mu;             // one reduction scratch per device: reductions are serialised
   int num_sms = 148;
 };
+
+// launch argument for the next reduction on c (caller holds c->red_mu)
+RedOut red_out(DevCtx* c);
+// wait for that reduction's results (spins on the mapped sequence word)
+int red_wait(DevCtx* c, const RedOut& ro, double* out, int k);
 
 int ctx_get(int device, DevCtx** out);  // initialises lazily, sets current device
 
@@ -75,6 +95,12 @@ struct sk_state {
 namespace sk {
 
 int state_alloc(int width, int dtype, int device, sk_state** out);
+// width-1 state from host amplitudes (re0, im0, re1, im1) whose Bloch sums the
+// kernel publishes to mapped memory (d_out4, then *d_flag = seq)
+int create_single_with_sums(int dtype, int device, const double amps[4], double* d_out4,
+                            unsigned long long* d_flag, unsigned long long seq, sk_state** out);
+// spin until a kernel publishes `seq` into the mapped word hflag (stream errors surface)
+int wait_mapped(int device, volatile unsigned long long* hflag, unsigned long long seq);
 inline size_t elem_size(int dtype) { return dtype == SK_C64 ? 8 : 16; }
 
 // ---------------------------------------------------------------------------

@@ -8,6 +8,8 @@
 // Reference semantics are cited per kernel (paths relative to
 // /root/reference/pkg/src/shardsim).
 #include <algorithm>
+#include <atomic>
+#include <cstring>
 #include <vector>
 
 #include "sk_internal.cuh"
@@ -52,7 +54,9 @@ int ctx_get(int device, DevCtx** out) {
       SK_CUDA(cudaStreamCreateWithFlags(&c.own_stream, cudaStreamNonBlocking));
       c.stream = c.own_stream;
       SK_CUDA(cudaMalloc(&c.d_partials, sizeof(double) * kRedMaxBlocks * kRedMaxK));
-      SK_CUDA(cudaMalloc(&c.d_result, sizeof(double) * kRedMaxK));
+      SK_CUDA(cudaHostAlloc(&c.h_map, sizeof(double) * (kRedMaxK + 1), cudaHostAllocMapped));
+      SK_CUDA(cudaHostGetDevicePointer((void**)&c.d_map, c.h_map, 0));
+      memset(c.h_map, 0, sizeof(double) * (kRedMaxK + 1));
       SK_CUDA(cudaMalloc(&c.d_counter, sizeof(unsigned int)));
       SK_CUDA(cudaMemset(c.d_counter, 0, sizeof(unsigned int)));
       SK_CUDA(cudaMallocHost(&c.h_result, sizeof(double) * kRedMaxK));
@@ -112,6 +116,49 @@ int state_alloc(int width, int dtype, int device, sk_state** out) {
   return SK_OK;
 }
 
+template <typename R>
+__global__ void k_set_single(vec2_t<R>* d, double ar, double ai, double br, double bi, double* out4,
+                             unsigned long long* flag, unsigned long long seq);
+
+int create_single_with_sums(int dtype, int device, const double amps[4], double* d_out4,
+                            unsigned long long* d_flag, unsigned long long seq, sk_state** out) {
+  sk_state* s;
+  SK_TRY(state_alloc(1, dtype, device, &s));
+  DevCtx* c;
+  SK_TRY(ctx_get(device, &c));
+  if (dtype == SK_C64)
+    k_set_single<float><<<1, 1, 0, c->stream>>>((float2*)s->d, amps[0], amps[1], amps[2], amps[3], d_out4, d_flag,
+                                                seq);
+  else
+    k_set_single<double><<<1, 1, 0, c->stream>>>((double2*)s->d, amps[0], amps[1], amps[2], amps[3], d_out4, d_flag,
+                                                  seq);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    sk_destroy(s);
+    return set_error(SK_ECUDA, "k_set_single: %s", cudaGetErrorString(e));
+  }
+  *out = s;
+  return SK_OK;
+}
+
+int wait_mapped(int device, volatile unsigned long long* hflag, unsigned long long seq) {
+  DevCtx* c;
+  SK_TRY(ctx_get(device, &c));
+  for (long it = 1; *hflag < seq; ++it) {  // sequence words only grow
+    if ((it & 4095) == 0) {
+      cudaError_t e = cudaStreamQuery(c->stream);
+      if (e == cudaSuccess) {
+        if (*hflag >= seq) break;
+        return set_error(SK_ECUDA, "mapped result %llu never published", seq);
+      }
+      if (e != cudaErrorNotReady) return set_error(SK_ECUDA, "stream: %s", cudaGetErrorString(e));
+      if (it > (1l << 22)) SK_CUDA(cudaStreamSynchronize(c->stream));
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
+  return SK_OK;
+}
+
 // tiny shards (the engine's width-1 qubits, engine.py:187-200) travel as a
 // kernel argument: no staging copy and no host wait
 struct SmallAmps {
@@ -128,8 +175,10 @@ __global__ void k_set_small(vec2_t<R>* d, int n, const __grid_constant__ SmallAm
 // reductions: K fp64 sums per launch, deterministic last-block combine
 // ---------------------------------------------------------------------------
 template <int K>
-__device__ __forceinline__ void block_reduce_finish(double (&v)[K], double* partials, unsigned* counter,
-                                                    double* result) {
+__device__ __forceinline__ void block_reduce_finish(double (&v)[K], const RedOut& ro) {
+  double* partials = ro.partials;
+  unsigned* counter = ro.counter;
+  double* result = ro.result;
   __shared__ double sh[32][K];
   __shared__ bool last;
 #pragma unroll
@@ -186,26 +235,69 @@ __device__ __forceinline__ void block_reduce_finish(double (&v)[K], double* part
       for (int off = 16; off > 0; off >>= 1) x += __shfl_down_sync(0xffffffffu, x, off);
       if (lane == 0) result[k] = x;
     }
-    if (lane == 0) *counter = 0;
+    if (lane == 0) {
+      *counter = 0;
+      __threadfence_system();  // the K results reach host memory before the sequence word
+      *(volatile unsigned long long*)ro.flag = ro.seq;
+    }
   }
 }
 
-template <int K>
-static int reduce_fetch(DevCtx* c, double* out) {
+RedOut red_out(DevCtx* c) {
+  RedOut ro;
+  ro.partials = c->d_partials;
+  ro.counter = c->d_counter;
+  ro.result = c->d_map;
+  ro.flag = (unsigned long long*)(c->d_map + kRedMaxK);
+  ro.seq = ++c->seq;
+  return ro;
+}
+
+int red_wait(DevCtx* c, const RedOut& ro, double* out, int k) {
   SK_CHECK_LAUNCH();
-  SK_CUDA(cudaMemcpyAsync(c->h_result, c->d_result, sizeof(double) * K, cudaMemcpyDeviceToHost, c->stream));
-  SK_CUDA(cudaStreamSynchronize(c->stream));
-  for (int k = 0; k < K; ++k) out[k] = c->h_result[k];
+  SK_TRY(wait_mapped(c->device, (volatile unsigned long long*)(c->h_map + kRedMaxK), ro.seq));
+  for (int i = 0; i < k; ++i) out[i] = ((volatile double*)c->h_map)[i];
   return SK_OK;
+}
+
+template <int K>
+static int reduce_fetch(DevCtx* c, const RedOut& ro, double* out) {
+  return red_wait(c, ro, out, K);
 }
 
 constexpr int kThreads = 256;
 constexpr int kUnroll = 4;
 
+// one (a0, a1) pair's contribution to the Bloch sums; shared by k_bloch and
+// k_set_single so a width-1 shard's cached sums are bit-identical to a reduction
+__device__ __forceinline__ void bloch_acc(double (&v)[4], double ar, double ai, double br, double bi) {
+  v[0] += ar * br + ai * bi;  // Re conj(a)*b
+  v[1] += ar * bi - ai * br;  // Im conj(a)*b
+  v[2] += ar * ar + ai * ai;
+  v[3] += br * br + bi * bi;
+}
+
+// a width-1 shard from two host amplitudes, plus its Bloch sums (as k_bloch
+// would reduce them from the stored precision) published to mapped host
+// memory with a sequence word: the hybrid engine's control elimination
+// (engine.py:407-436) then reads them without a device round trip
+template <typename R>
+__global__ void k_set_single(vec2_t<R>* d, double ar, double ai, double br, double bi, double* out4,
+                             unsigned long long* flag, unsigned long long seq) {
+  const vec2_t<R> a = mk<R>((R)ar, (R)ai), b = mk<R>((R)br, (R)bi);
+  d[0] = a;
+  d[1] = b;
+  double v[4] = {0, 0, 0, 0};
+  bloch_acc(v, a.x, a.y, b.x, b.y);
+  for (int k = 0; k < 4; ++k) out4[k] = v[k];
+  __threadfence_system();
+  *(volatile unsigned long long*)flag = seq;
+}
+
 // bloch_vector (ket.py:204-210): sum conj(a0)*a1, sum |a0|^2, sum |a1|^2
 template <typename R>
 __global__ void __launch_bounds__(kThreads) k_bloch(const vec2_t<R>* __restrict__ a, int64_t npairs, int q,
-                                                   double* partials, unsigned* counter, double* result) {
+                                                   RedOut ro) {
   double v[4] = {0, 0, 0, 0};
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const uint64_t bit = 1ull << q;
@@ -224,20 +316,13 @@ __global__ void __launch_bounds__(kThreads) k_bloch(const vec2_t<R>* __restrict_
       }
     }
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      double ar = x0[u].x, ai = x0[u].y, br = x1[u].x, bi = x1[u].y;
-      v[0] += ar * br + ai * bi;  // Re conj(a)*b
-      v[1] += ar * bi - ai * br;  // Im conj(a)*b
-      v[2] += ar * ar + ai * ai;
-      v[3] += br * br + bi * bi;
-    }
+    for (int u = 0; u < kUnroll; ++u) bloch_acc(v, x0[u].x, x0[u].y, x1[u].x, x1[u].y);
   }
-  block_reduce_finish<4>(v, partials, counter, result);
+  block_reduce_finish<4>(v, ro);
 }
 
 template <typename R>
-__global__ void __launch_bounds__(kThreads) k_norm2(const vec2_t<R>* __restrict__ a, int64_t n, double* partials,
-                                                   unsigned* counter, double* result) {
+__global__ void __launch_bounds__(kThreads) k_norm2(const vec2_t<R>* __restrict__ a, int64_t n, RedOut ro) {
   double v[1] = {0};
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += kUnroll * stride) {
@@ -250,12 +335,12 @@ __global__ void __launch_bounds__(kThreads) k_norm2(const vec2_t<R>* __restrict_
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) v[0] += (double)x[u].x * x[u].x + (double)x[u].y * x[u].y;
   }
-  block_reduce_finish<1>(v, partials, counter, result);
+  block_reduce_finish<1>(v, ro);
 }
 
 template <typename R>
 __global__ void __launch_bounds__(kThreads) k_vdot(const vec2_t<R>* __restrict__ a, const vec2_t<R>* __restrict__ b,
-                                                  int64_t n, double* partials, unsigned* counter, double* result) {
+                                                  int64_t n, RedOut ro) {
   double v[2] = {0, 0};
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += kUnroll * stride) {
@@ -273,7 +358,7 @@ __global__ void __launch_bounds__(kThreads) k_vdot(const vec2_t<R>* __restrict__
       v[1] += ar * bi - ai * br;
     }
   }
-  block_reduce_finish<2>(v, partials, counter, result);
+  block_reduce_finish<2>(v, ro);
 }
 
 // ---------------------------------------------------------------------------
@@ -368,8 +453,7 @@ __global__ void __launch_bounds__(kThreads) k_apply_ctrl(vec2_t<R>* __restrict__
 // (engine.py:389-394 runs apply_controlled then bloch_vector twice).
 template <typename R>
 __global__ void __launch_bounds__(kThreads) k_ctrl_bloch(vec2_t<R>* __restrict__ a, int64_t nquads, int c, int pol,
-                                                        int t, Mat2<R> m, double* partials, unsigned* counter,
-                                                        double* result) {
+                                                        int t, Mat2<R> m, RedOut ro) {
   double v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const uint64_t C = 1ull << c, T = 1ull << t;
@@ -405,7 +489,7 @@ __global__ void __launch_bounds__(kThreads) k_ctrl_bloch(vec2_t<R>* __restrict__
       v[3] += br * br + bi * bi;
     }
   }
-  block_reduce_finish<8>(v, partials, counter, result);
+  block_reduce_finish<8>(v, ro);
 }
 
 // apply_pauli_layer (ket.py:166-202), in place (the reference gathers out of
@@ -920,11 +1004,13 @@ int sk_apply_controlled_bloch(sk_state* s, int control, int polarity, int target
   SK_TRY(ctx_get(s->device, &c));
   const int64_t nq = s->n / 4;
   const int g = grid_for(nq, kThreads, 2, c->num_sms);
+  std::lock_guard<std::mutex> lk(c->red_mu);
   return dispatch(s, [&](auto r) {
     using R = decltype(r);
+    const RedOut ro = red_out(c);
     k_ctrl_bloch<R><<<g, kThreads, 0, c->stream>>>((vec2_t<R>*)s->d, nq, control, polarity, target, mat_from<R>(m),
-                                                   c->d_partials, c->d_counter, c->d_result);
-    return reduce_fetch<8>(c, out8);
+                                                   ro);
+    return reduce_fetch<8>(c, ro, out8);
   });
 }
 
@@ -982,11 +1068,12 @@ int sk_bloch_sums(const sk_state* s, int q, double out4[4]) {
   SK_TRY(ctx_get(s->device, &c));
   const int64_t np_ = s->n / 2;
   const int g = grid_for(np_, kThreads, kUnroll, c->num_sms);
+  std::lock_guard<std::mutex> lk(c->red_mu);
   return dispatch(s, [&](auto r) {
     using R = decltype(r);
-    k_bloch<R><<<g, kThreads, 0, c->stream>>>((const vec2_t<R>*)s->d, np_, q, c->d_partials, c->d_counter,
-                                              c->d_result);
-    return reduce_fetch<4>(c, out4);
+    const RedOut ro = red_out(c);
+    k_bloch<R><<<g, kThreads, 0, c->stream>>>((const vec2_t<R>*)s->d, np_, q, ro);
+    return reduce_fetch<4>(c, ro, out4);
   });
 }
 
@@ -995,11 +1082,12 @@ int sk_norm2(const sk_state* s, double* out) {
   DevCtx* c;
   SK_TRY(ctx_get(s->device, &c));
   const int g = grid_for(s->n, kThreads, kUnroll, c->num_sms);
+  std::lock_guard<std::mutex> lk(c->red_mu);
   return dispatch(s, [&](auto r) {
     using R = decltype(r);
-    k_norm2<R><<<g, kThreads, 0, c->stream>>>((const vec2_t<R>*)s->d, s->n, c->d_partials, c->d_counter,
-                                              c->d_result);
-    return reduce_fetch<1>(c, out);
+    const RedOut ro = red_out(c);
+    k_norm2<R><<<g, kThreads, 0, c->stream>>>((const vec2_t<R>*)s->d, s->n, ro);
+    return reduce_fetch<1>(c, ro, out);
   });
 }
 
@@ -1012,11 +1100,12 @@ int sk_vdot(const sk_state* a, const sk_state* b, double out2[2]) {
   DevCtx* c;
   SK_TRY(ctx_get(a->device, &c));
   const int g = grid_for(a->n, kThreads, kUnroll, c->num_sms);
+  std::lock_guard<std::mutex> lk(c->red_mu);
   return dispatch(a, [&](auto r) {
     using R = decltype(r);
-    k_vdot<R><<<g, kThreads, 0, c->stream>>>((const vec2_t<R>*)a->d, (const vec2_t<R>*)b->d, a->n, c->d_partials,
-                                             c->d_counter, c->d_result);
-    return reduce_fetch<2>(c, out2);
+    const RedOut ro = red_out(c);
+    k_vdot<R><<<g, kThreads, 0, c->stream>>>((const vec2_t<R>*)a->d, (const vec2_t<R>*)b->d, a->n, ro);
+    return reduce_fetch<2>(c, ro, out2);
   });
 }
 

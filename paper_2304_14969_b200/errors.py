@@ -24,3 +24,9 @@ class InvariantError(RuntimeError):
 
 class DeviceError(RuntimeError):
     """A CUDA runtime failure inside libshardcu."""
+
+
+class DeviceMemoryError(DeviceError, MemoryError):
+    """The device itself ran out of memory (cudaMalloc failed).  Distinct from
+    MemoryBudgetError: a search that treats a budget error as "p too low"
+    (validate.py:292-294) must not mistake a full GPU for it."""

@@ -115,10 +115,10 @@ class DenseKet:
     Single-writer contract: one mutating operation at a time per shard.
     """
 
-    __slots__ = ("width", "dtype", "device", "_h", "__weakref__")
+    __slots__ = ("width", "dtype", "device", "_h", "_owned", "__weakref__")
 
     def __init__(self, width: int, amps: np.ndarray | None = None, *, dtype: str | None = None,
-                 device: int | None = None, _handle=None):
+                 device: int | None = None, _handle=None, _borrowed: bool = False):
         global alloc_count
         if width < 1:
             raise ValueError("shard width must be >= 1")
@@ -126,6 +126,7 @@ class DenseKet:
         self.dtype = _default_dtype if dtype is None else ("c64" if _lib.DTYPES[dtype] == _lib.SK_C64 else "c128")
         self.device = _default_device if device is None else int(device)
         self._h = None
+        self._owned = not _borrowed
         code = _lib.DTYPES[self.dtype]
         h = C.c_void_p()
         if _handle is not None:
@@ -141,11 +142,12 @@ class DenseKet:
             call("sk_create_from", width, code, self.device, buf.ctypes.data_as(_lib.dptr), C.byref(h),
                  needed=1 << width)
         self._h = h
-        alloc_count += 1
+        if not _borrowed:
+            alloc_count += 1
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and _lib._lib is not None:
+        if h is not None and _lib._lib is not None and getattr(self, "_owned", True):
             try:
                 _lib._lib.sk_destroy(h)
             except Exception:
