@@ -38,11 +38,30 @@ def headers() -> list[Path]:
     return sorted(CSRC.glob("*.cuh")) + sorted(INCLUDE.glob("*.h"))
 
 
+def _deps(src: Path, seen: set | None = None) -> set:
+    """src plus every header it #includes (transitively) from csrc/ and include/."""
+    import re
+    seen = set() if seen is None else seen
+    if src in seen or not src.exists():
+        return seen
+    seen.add(src)
+    for inc in re.findall(r'#include\s+"([^"]+)"', src.read_text(errors="ignore")):
+        _deps((src.parent / inc).resolve(), seen)
+    return seen
+
+
 def is_stale() -> bool:
     if not LIB.exists():
         return True
     t = LIB.stat().st_mtime
     return any(p.stat().st_mtime > t for p in sources() + headers())
+
+
+def _obj_stale(src: Path, obj: Path) -> bool:
+    if not obj.exists():
+        return True
+    t = obj.stat().st_mtime
+    return any(p.stat().st_mtime > t for p in _deps(src.resolve()))
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
@@ -54,6 +73,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
 
     def compile_one(src: Path) -> Path:
         obj = objdir / (src.stem + ".o")
+        if not force and not _obj_stale(src, obj):
+            return obj  # incremental: only sources whose own include closure changed
         cmd = [nvcc, *ARCH, *FLAGS, "-c", str(src), "-o", str(obj)]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)

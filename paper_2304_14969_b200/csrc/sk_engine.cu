@@ -34,6 +34,7 @@
 #include <vector>
 
 #include "sk_internal.cuh"
+#include "sk_ops.cuh"
 
 namespace {
 
@@ -209,7 +210,109 @@ struct Qubit {
 
 }  // namespace
 
+// ---------------------------------------------------------------------------
+// engine kernels.  Every element operation and reduction is the shared one
+// of sk_ops.cuh, so results are bit-identical to the separate ket kernels
+// (k_apply_1q, k_kron, k_ctrl_bloch, k_round, k_set_single) they fuse.
+// ---------------------------------------------------------------------------
+namespace sk {
+
+constexpr int kEThreads = 256;
+// widths whose one-control gate k_ctrl_bloch reduces in a single block
+// (2^(w-2) quads <= 256 threads x 2): the fused coupler kernel keeps its
+// summation order
+constexpr int kFusedMaxW = 11;
+
+template <typename R>
+__device__ __forceinline__ Mat2<R> dmat(const double* m) {
+  Mat2<R> r;
+  r.m00 = mk<R>((R)m[0], (R)m[1]);
+  r.m01 = mk<R>((R)m[2], (R)m[3]);
+  r.m10 = mk<R>((R)m[4], (R)m[5]);
+  r.m11 = mk<R>((R)m[6], (R)m[7]);
+  return r;
+}
+
+struct CouplerArgs {
+  void* pre_ptr[2];  // committed 1q buffers (engine.py:376 -> :305-322), in order
+  int pre_w[2], pre_q[2], pre_diag[2];
+  double pre_m[2][8];
+  int npre;
+  const void* lo;    // merge (engine.py:224-243): out = kron(hi, lo); lo == nullptr: no merge
+  const void* hi;
+  int wa, wb;
+  void* out;         // the state the gate acts on
+  int c, pol, t, w;
+  double m[8];
+};
+
+// A committed one-control coupler on a small shard, one block: the operands'
+// 1q buffers, the Kronecker merge, the gate and both operands' Bloch sums
+// (engine.py:367-394) in one launch.
+template <typename R>
+__global__ void __launch_bounds__(kEThreads) k_e_coupler(const __grid_constant__ CouplerArgs A, RedOut ro) {
+  const int tid = threadIdx.x;
+  for (int i = 0; i < A.npre; ++i) {
+    vec2_t<R>* a = (vec2_t<R>*)A.pre_ptr[i];
+    const Mat2<R> m = dmat<R>(A.pre_m[i]);
+    const int64_t np = int64_t(1) << (A.pre_w[i] - 1);
+    const uint64_t bit = 1ull << A.pre_q[i];
+    for (int64_t k = tid; k < np; k += kEThreads) apply_1q_pair<R>(a, insert0(k, A.pre_q[i]), bit, m, A.pre_diag[i]);
+    __syncthreads();
+  }
+  vec2_t<R>* s = (vec2_t<R>*)A.out;
+  if (A.lo) {
+    const vec2_t<R>* lo = (const vec2_t<R>*)A.lo;
+    const vec2_t<R>* hi = (const vec2_t<R>*)A.hi;
+    const int64_t n = int64_t(1) << (A.wa + A.wb);
+    const uint64_t mask = (1ull << A.wa) - 1;
+    for (int64_t i = tid; i < n; i += kEThreads) s[i] = cmul<R>(hi[(uint64_t)i >> A.wa], lo[(uint64_t)i & mask]);
+    __syncthreads();
+  }
+  double v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const Mat2<R> m = dmat<R>(A.m);
+  const uint64_t C = 1ull << A.c, T = 1ull << A.t;
+  const int lo_b = A.c < A.t ? A.c : A.t, hi_b = A.c < A.t ? A.t : A.c;
+  const int64_t nq = int64_t(1) << (A.w - 2);
+  for (int64_t k = tid; k < nq; k += kEThreads) ctrl_bloch_quad<R>(s, insert0(insert0(k, lo_b), hi_b), C, T, A.pol, m, v);
+  block_reduce_finish<8>(v, ro);
+}
+
+// kron_compose (ket.py:239-241) into a caller-provided buffer
+template <typename R>
+__global__ void __launch_bounds__(kEThreads) k_e_kron(const vec2_t<R>* __restrict__ lo, const vec2_t<R>* __restrict__ hi,
+                                                     vec2_t<R>* __restrict__ out, int64_t n, int wa) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const uint64_t mask = (1ull << wa) - 1;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = cmul<R>(hi[(uint64_t)i >> wa], lo[(uint64_t)i & mask]);
+}
+
+// SDRP rounding split (engine.py:464-488) in one launch: the remainder
+// rest[k] = (u00 a0[k] + u01 a1[k]) / sqrt(P0) and the new width-1 shard phi
+// with its published Bloch sums
+template <typename R>
+__global__ void __launch_bounds__(kEThreads) k_e_round_split(const vec2_t<R>* __restrict__ a, vec2_t<R>* __restrict__ out,
+                                                            int64_t nout, int q, vec2_t<R> u00, vec2_t<R> u01, R scale,
+                                                            vec2_t<R>* single, double p0r, double p0i, double p1r,
+                                                            double p1i, double* out4, unsigned long long* flag,
+                                                            unsigned long long seq) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const uint64_t bit = 1ull << q;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nout; k += stride) {
+    uint64_t i0 = insert0(k, q);
+    vec2_t<R> y = cmad2<R>(u00, a[i0], u01, a[i0 | bit]);
+    out[k] = mk<R>(y.x * scale, y.y * scale);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) publish_single<R>(single, p0r, p0i, p1r, p1i, out4, flag, seq);
+}
+
+}  // namespace sk
+
 using namespace sk;
+
+constexpr int kPoolMaxW = 18;   // cache freed shard buffers up to 4 MiB (c128)
+constexpr size_t kPoolPerW = 32;
 
 struct sk_engine {
   int n = 0;
@@ -228,6 +331,8 @@ struct sk_engine {
   double* d_ring = nullptr;
   int ring_next = 0;
   unsigned long long ring_seq = 0;
+  std::vector<void*> pool[kPoolMaxW + 1];  // freed shard buffers by width (stream-ordered reuse)
+  DevCtx* ctx = nullptr;
 
   ~sk_engine() {
     std::unordered_set<PendingOp*> ops;
@@ -238,16 +343,56 @@ struct sk_engine {
       sk_destroy(s->st);
       delete s;
     }
-    if (h_ring) {
-      DevCtx* c;
-      if (ctx_get(cfg.device, &c) == SK_OK) cudaStreamSynchronize(c->stream);  // kernels may still publish
-      cudaFreeHost(h_ring);
+    DevCtx* c;
+    if (ctx_get(cfg.device, &c) == SK_OK) {
+      for (auto& v : pool)
+        for (void* p : v) cudaFreeAsync(p, c->stream);
+      if (h_ring) cudaStreamSynchronize(c->stream);  // kernels may still publish
     }
+    if (h_ring) cudaFreeHost(h_ring);
+  }
+
+  // shard buffers: engine-side cache of freed device buffers per width, so
+  // the merge / split churn of small shards never reaches the driver
+  int alloc_state(int w, sk_state** out) {
+    if (w <= kPoolMaxW && !pool[w].empty()) {
+      sk_state* s = new sk_state();
+      s->width = w;
+      s->dtype = cfg.dtype;
+      s->device = cfg.device;
+      s->n = int64_t(1) << w;
+      s->elem = elem_size(cfg.dtype);
+      s->d = pool[w].back();
+      pool[w].pop_back();
+      *out = s;
+    } else {
+      SK_TRY(state_alloc(w, cfg.dtype, cfg.device, out));
+    }
+    stats[SK_ENGINE_STAT_ALLOCS]++;
+    return SK_OK;
+  }
+
+  void free_state(sk_state* s) {
+    if (!s) return;
+    if (s->owned && s->d && s->width <= kPoolMaxW && pool[s->width].size() < kPoolPerW) {
+      pool[s->width].push_back(s->d);
+      delete s;
+      return;
+    }
+    sk_destroy(s);
+  }
+
+  unsigned long long ring_ticket(double** dslot, int* slot) {
+    *slot = ring_next;
+    ring_next = (ring_next + 1) % kRingSlots;
+    *dslot = d_ring + (size_t)*slot * kSlotDoubles;
+    return ++ring_seq;
   }
 
   int init_ring() {
     DevCtx* c;
     SK_TRY(ctx_get(cfg.device, &c));
+    ctx = c;
     SK_CUDA(cudaHostAlloc(&h_ring, sizeof(double) * kRingSlots * kSlotDoubles, cudaHostAllocMapped));
     SK_CUDA(cudaHostGetDevicePointer((void**)&d_ring, h_ring, 0));
     memset(h_ring, 0, sizeof(double) * kRingSlots * kSlotDoubles);
@@ -283,7 +428,7 @@ struct sk_engine {
 
   void drop_shard(Shard* s) {
     shards.erase(s);
-    sk_destroy(s->st);
+    free_state(s->st);
     delete s;
   }
 
@@ -323,12 +468,27 @@ struct sk_engine {
 
   int merge_pair(Shard* a, Shard* b, Shard** out) {  // engine.py:224-243: the wider keeps its positions
     if (a->width() < b->width()) std::swap(a, b);
-    stats[SK_ENGINE_STAT_MERGES]++;
     const int wa = a->width(), wb = b->width();
     SK_TRY(charge(int64_t(1) << (wa + wb)));
     sk_state* st;
-    SK_TRY(sk_kron(a->st, b->st, &st));
-    stats[SK_ENGINE_STAT_ALLOCS]++;
+    SK_TRY(alloc_state(wa + wb, &st));
+    const int64_t n = int64_t(1) << (wa + wb);
+    const int g = grid_for(n, kEThreads, 2, ctx->num_sms);
+    if (cfg.dtype == SK_C64)
+      k_e_kron<float><<<g, kEThreads, 0, ctx->stream>>>((const float2*)a->st->d, (const float2*)b->st->d,
+                                                         (float2*)st->d, n, wa);
+    else
+      k_e_kron<double><<<g, kEThreads, 0, ctx->stream>>>((const double2*)a->st->d, (const double2*)b->st->d,
+                                                          (double2*)st->d, n, wa);
+    SK_CHECK_LAUNCH();
+    SK_TRY(merged_shard(a, b, st, out));
+    return SK_OK;
+  }
+
+  // bookkeeping of a merge whose product is already (being) written to st
+  int merged_shard(Shard* a, Shard* b, sk_state* st, Shard** out) {
+    const int wa = a->width(), wb = b->width();
+    stats[SK_ENGINE_STAT_MERGES]++;
     stats[SK_ENGINE_STAT_WRITES] += int64_t(1) << (wa + wb);
     SK_TRY(release((int64_t(1) << wa) + (int64_t(1) << wb)));
     Shard* m = new_shard(st);
@@ -366,7 +526,7 @@ struct sk_engine {
     q->pos = 0;
     shard->qubits.erase(shard->qubits.begin() + pos);
     for (int i = 0; i < shard->width(); ++i) shard->qubits[i]->pos = i;
-    sk_destroy(shard->st);
+    free_state(shard->st);
     shard->st = rest;
     shard->sums.kind = kSumsNone;
     dense_total += (2 + (int64_t(1) << rest->width)) - old;
@@ -509,34 +669,118 @@ struct sk_engine {
   int commit_ctrl(const std::vector<Qubit*>& controls, const std::vector<int>& pol, Qubit* target, const M2& m) {
     std::vector<Qubit*> qs = controls;
     qs.push_back(target);
-    for (Qubit* q : qs) SK_TRY(commit_1q(q));
-    Shard* s;
-    SK_TRY(merge_for(qs, &s));
-    if (!unitary(m)) return set_error(SK_EVALUE, "matrix is not unitary within 1e-10");
-    double m8[8];
-    m_to8(m, m8);
-    std::vector<std::vector<double>> pre;
-    if (controls.size() == 1) {
-      double out8[8];
-      SK_TRY(sk_apply_controlled_bloch(s->st, controls[0]->pos, pol[0], target->pos, m8, out8));
-      pre = {std::vector<double>(out8, out8 + 4), std::vector<double>(out8 + 4, out8 + 8)};
-      stats[SK_ENGINE_STAT_WRITES] += int64_t(1) << (s->width() - 1);
-    } else {
-      uint64_t mask = 0, val = 0;
-      for (size_t i = 0; i < controls.size(); ++i) {
-        mask |= 1ull << controls[i]->pos;
-        if (pol[i]) val |= 1ull << controls[i]->pos;
+    double out8[8];
+    bool fused = false;
+    if (controls.size() == 1) SK_TRY(coupler_small(controls[0], pol[0], target, m, out8, &fused));
+    if (!fused) {
+      for (Qubit* q : qs) SK_TRY(commit_1q(q));
+      Shard* s;
+      SK_TRY(merge_for(qs, &s));
+      if (!unitary(m)) return set_error(SK_EVALUE, "matrix is not unitary within 1e-10");
+      double m8[8];
+      m_to8(m, m8);
+      if (controls.size() == 1) {
+        SK_TRY(sk_apply_controlled_bloch(s->st, controls[0]->pos, pol[0], target->pos, m8, out8));
+        stats[SK_ENGINE_STAT_WRITES] += int64_t(1) << (s->width() - 1);
+      } else {
+        uint64_t mask = 0, val = 0;
+        for (size_t i = 0; i < controls.size(); ++i) {
+          mask |= 1ull << controls[i]->pos;
+          if (pol[i]) val |= 1ull << controls[i]->pos;
+        }
+        SK_TRY(sk_apply_controlled(s->st, mask, val, target->pos, m8));
+        stats[SK_ENGINE_STAT_WRITES] += 2 * (int64_t(1) << (s->width() - 1 - (int)controls.size()));
       }
-      SK_TRY(sk_apply_controlled(s->st, mask, val, target->pos, m8));
-      stats[SK_ENGINE_STAT_WRITES] += 2 * (int64_t(1) << (s->width() - 1 - (int)controls.size()));
+      s->sums.kind = kSumsNone;
+      stats[SK_ENGINE_STAT_KERNELS]++;
     }
-    s->sums.kind = kSumsNone;
-    stats[SK_ENGINE_STAT_KERNELS]++;
+    const double* pre = controls.size() == 1 ? out8 : nullptr;
     for (size_t i = 0; i < qs.size(); ++i) {
       bool changed = false;
-      SK_TRY(try_factor(qs[i], pre.empty() ? nullptr : pre[i].data(), &changed));
-      if (changed) pre.clear();  // later operands see a new state: recompute their sums
+      SK_TRY(try_factor(qs[i], pre ? pre + 4 * i : nullptr, &changed));
+      if (changed) pre = nullptr;  // later operands see a new state: recompute their sums
     }
+    return SK_OK;
+  }
+
+  // The one-control coupler on shards whose merged width is small, as ONE
+  // launch (k_e_coupler): commit the operands' 1q buffers (engine.py:376),
+  // merge (engine.py:377, :224-243), apply the gate and return both operands'
+  // Bloch sums.  Bookkeeping and budget checks run in the reference's order;
+  // *fused = false leaves everything to the general path.
+  int coupler_small(Qubit* c, int pol, Qubit* t, const M2& m, double out8[8], bool* fused) {
+    *fused = false;
+    Shard *sa = c->shard, *sb = t->shard;
+    const bool merge = sa != sb;
+    const int w = merge ? sa->width() + sb->width() : sa->width();
+    if (w > kFusedMaxW) return SK_OK;
+    CouplerArgs A{};
+    for (Qubit* q : {c, t}) {  // commit_1q of each operand (engine.py:305-322)
+      if (!q->has_u) continue;
+      const M2 u = q->u;
+      q->has_u = false;
+      if (is_identity(u)) continue;
+      if (!unitary(u)) return set_error(SK_EVALUE, "matrix is not unitary within 1e-10");
+      const int i = A.npre++;
+      A.pre_ptr[i] = q->shard->st->d;
+      A.pre_w[i] = q->shard->width();
+      A.pre_q[i] = q->pos;
+      m_to8(u, A.pre_m[i]);
+      A.pre_diag[i] = (A.pre_m[i][2] == 0.0 && A.pre_m[i][3] == 0.0 && A.pre_m[i][4] == 0.0 && A.pre_m[i][5] == 0.0);
+      stats[SK_ENGINE_STAT_KERNELS]++;
+      stats[SK_ENGINE_STAT_WRITES] += int64_t(1) << q->shard->width();
+      q->shard->sums.kind = kSumsNone;
+    }
+    Shard *lo = sa, *hi = sb;
+    sk_state* st = sa->st;
+    if (merge) {
+      if (lo->width() < hi->width()) std::swap(lo, hi);
+      int rc = charge(int64_t(1) << w);
+      if (rc != SK_OK) {  // the reference committed the buffers before its budget check
+        for (int i = 0; i < A.npre; ++i) {
+          sk_state tmp;
+          tmp.d = A.pre_ptr[i];
+          tmp.width = A.pre_w[i];
+          tmp.dtype = cfg.dtype;
+          tmp.device = cfg.device;
+          tmp.n = int64_t(1) << A.pre_w[i];
+          tmp.elem = elem_size(cfg.dtype);
+          SK_TRY(sk_apply_1q(&tmp, A.pre_q[i], A.pre_m[i]));
+        }
+        return rc;
+      }
+      SK_TRY(alloc_state(w, &st));
+      A.lo = lo->st->d;
+      A.hi = hi->st->d;
+      A.wa = lo->width();
+      A.wb = hi->width();
+    }
+    if (!unitary(m)) return set_error(SK_EVALUE, "matrix is not unitary within 1e-10");
+    A.out = st->d;
+    A.w = w;
+    A.pol = pol;
+    m_to8(m, A.m);
+    if (merge) {  // positions in the merged shard: the wider keeps its own
+      A.c = c->shard == lo ? c->pos : lo->width() + c->pos;
+      A.t = t->shard == lo ? t->pos : lo->width() + t->pos;
+    } else {
+      A.c = c->pos;
+      A.t = t->pos;
+    }
+    std::lock_guard<std::mutex> lk(ctx->red_mu);
+    const RedOut ro = red_out(ctx);
+    if (cfg.dtype == SK_C64)
+      k_e_coupler<float><<<1, kEThreads, 0, ctx->stream>>>(A, ro);
+    else
+      k_e_coupler<double><<<1, kEThreads, 0, ctx->stream>>>(A, ro);
+    SK_CHECK_LAUNCH();
+    Shard* s = sa;
+    if (merge) SK_TRY(merged_shard(lo, hi, st, &s));
+    stats[SK_ENGINE_STAT_WRITES] += int64_t(1) << (w - 1);
+    stats[SK_ENGINE_STAT_KERNELS]++;
+    s->sums.kind = kSumsNone;
+    SK_TRY(red_wait(ctx, ro, out8, 8));
+    *fused = true;
     return SK_OK;
   }
 
@@ -608,14 +852,30 @@ struct sk_engine {
     const double p0 = std::norm(u.a[0]) * sums[2] + std::norm(u.a[1]) * sums[3] +
                       2.0 * (std::conj(u.a[0]) * u.a[1] * cross).real();
     if (p0 < 1e-12) return SK_OK;  // numerically degenerate: leave the state alone (engine.py:477-480)
-    const double u0[4] = {u.a[0].real(), u.a[0].imag(), u.a[1].real(), u.a[1].imag()};
-    sk_state* rest;
-    SK_TRY(sk_round_compact(shard->st, pos, u0, 1.0 / std::sqrt(p0), &rest));
-    stats[SK_ENGINE_STAT_ALLOCS]++;
-    stats[SK_ENGINE_STAT_WRITES] += int64_t(1) << shard->width();
-    sk_state* single;
+    const int w = shard->width();
+    sk_state *rest, *single;
+    SK_TRY(alloc_state(w - 1, &rest));
+    SK_TRY(alloc_state(1, &single));
     SumsTicket ss;
-    SK_TRY(make_single(phi, &single, &ss));
+    double* dslot;
+    ss.kind = kSumsSlot;
+    ss.seq = ring_ticket(&dslot, &ss.slot);
+    const int64_t nout = int64_t(1) << (w - 1);
+    const int g = grid_for(nout, kEThreads, 2, ctx->num_sms);
+    const double scale = 1.0 / std::sqrt(p0);
+    unsigned long long* dflag = (unsigned long long*)(dslot + 4);
+    if (cfg.dtype == SK_C64)
+      k_e_round_split<float><<<g, kEThreads, 0, ctx->stream>>>(
+          (const float2*)shard->st->d, (float2*)rest->d, nout, pos, mk<float>((float)u.a[0].real(), (float)u.a[0].imag()),
+          mk<float>((float)u.a[1].real(), (float)u.a[1].imag()), (float)scale, (float2*)single->d, phi[0].real(),
+          phi[0].imag(), phi[1].real(), phi[1].imag(), dslot, dflag, ss.seq);
+    else
+      k_e_round_split<double><<<g, kEThreads, 0, ctx->stream>>>(
+          (const double2*)shard->st->d, (double2*)rest->d, nout, pos, mk<double>(u.a[0].real(), u.a[0].imag()),
+          mk<double>(u.a[1].real(), u.a[1].imag()), scale, (double2*)single->d, phi[0].real(), phi[0].imag(),
+          phi[1].real(), phi[1].imag(), dslot, dflag, ss.seq);
+    SK_CHECK_LAUNCH();
+    stats[SK_ENGINE_STAT_WRITES] += int64_t(1) << w;
     split(shard, pos, single, ss, rest);
     if (eps > cfg.separability_tol) eps_push(eps);
     *rounded = true;

@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "sk_internal.cuh"
+#include "sk_ops.cuh"
 
 namespace sk {
 
@@ -171,78 +172,6 @@ __global__ void k_set_small(vec2_t<R>* d, int n, const __grid_constant__ SmallAm
   if (i < n) d[i] = mk<R>((R)a.v[2 * i], (R)a.v[2 * i + 1]);
 }
 
-// ---------------------------------------------------------------------------
-// reductions: K fp64 sums per launch, deterministic last-block combine
-// ---------------------------------------------------------------------------
-template <int K>
-__device__ __forceinline__ void block_reduce_finish(double (&v)[K], const RedOut& ro) {
-  double* partials = ro.partials;
-  unsigned* counter = ro.counter;
-  double* result = ro.result;
-  __shared__ double sh[32][K];
-  __shared__ bool last;
-#pragma unroll
-  for (int k = 0; k < K; ++k) {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v[k] += __shfl_down_sync(0xffffffffu, v[k], off);
-  }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
-  if (lane == 0) {
-#pragma unroll
-    for (int k = 0; k < K; ++k) sh[warp][k] = v[k];
-  }
-  __syncthreads();
-  if (warp == 0) {
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      double x = lane < nw ? sh[lane][k] : 0.0;
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) x += __shfl_down_sync(0xffffffffu, x, off);
-      if (lane == 0) partials[blockIdx.x * K + k] = x;
-    }
-  }
-  if (threadIdx.x == 0) {
-    __threadfence();
-    unsigned prev = atomicAdd(counter, 1u);
-    last = (prev == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  double acc[K];
-#pragma unroll
-  for (int k = 0; k < K; ++k) acc[k] = 0.0;
-  for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
-#pragma unroll
-    for (int k = 0; k < K; ++k) acc[k] += ((volatile double*)partials)[b * K + k];
-  }
-#pragma unroll
-  for (int k = 0; k < K; ++k) {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) acc[k] += __shfl_down_sync(0xffffffffu, acc[k], off);
-  }
-  __syncthreads();
-  if (lane == 0) {
-#pragma unroll
-    for (int k = 0; k < K; ++k) sh[warp][k] = acc[k];
-  }
-  __syncthreads();
-  if (warp == 0) {
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      double x = lane < nw ? sh[lane][k] : 0.0;
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) x += __shfl_down_sync(0xffffffffu, x, off);
-      if (lane == 0) result[k] = x;
-    }
-    if (lane == 0) {
-      *counter = 0;
-      __threadfence_system();  // the K results reach host memory before the sequence word
-      *(volatile unsigned long long*)ro.flag = ro.seq;
-    }
-  }
-}
-
 RedOut red_out(DevCtx* c) {
   RedOut ro;
   ro.partials = c->d_partials;
@@ -268,15 +197,6 @@ static int reduce_fetch(DevCtx* c, const RedOut& ro, double* out) {
 constexpr int kThreads = 256;
 constexpr int kUnroll = 4;
 
-// one (a0, a1) pair's contribution to the Bloch sums; shared by k_bloch and
-// k_set_single so a width-1 shard's cached sums are bit-identical to a reduction
-__device__ __forceinline__ void bloch_acc(double (&v)[4], double ar, double ai, double br, double bi) {
-  v[0] += ar * br + ai * bi;  // Re conj(a)*b
-  v[1] += ar * bi - ai * br;  // Im conj(a)*b
-  v[2] += ar * ar + ai * ai;
-  v[3] += br * br + bi * bi;
-}
-
 // a width-1 shard from two host amplitudes, plus its Bloch sums (as k_bloch
 // would reduce them from the stored precision) published to mapped host
 // memory with a sequence word: the hybrid engine's control elimination
@@ -284,14 +204,7 @@ __device__ __forceinline__ void bloch_acc(double (&v)[4], double ar, double ai, 
 template <typename R>
 __global__ void k_set_single(vec2_t<R>* d, double ar, double ai, double br, double bi, double* out4,
                              unsigned long long* flag, unsigned long long seq) {
-  const vec2_t<R> a = mk<R>((R)ar, (R)ai), b = mk<R>((R)br, (R)bi);
-  d[0] = a;
-  d[1] = b;
-  double v[4] = {0, 0, 0, 0};
-  bloch_acc(v, a.x, a.y, b.x, b.y);
-  for (int k = 0; k < 4; ++k) out4[k] = v[k];
-  __threadfence_system();
-  *(volatile unsigned long long*)flag = seq;
+  publish_single<R>(d, ar, ai, br, bi, out4, flag, seq);
 }
 
 // bloch_vector (ket.py:204-210): sum conj(a0)*a1, sum |a0|^2, sum |a1|^2
@@ -458,37 +371,8 @@ __global__ void __launch_bounds__(kThreads) k_ctrl_bloch(vec2_t<R>* __restrict__
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const uint64_t C = 1ull << c, T = 1ull << t;
   const int lo = c < t ? c : t, hi = c < t ? t : c;
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nquads; k += stride) {
-    uint64_t b = insert0(insert0(k, lo), hi);
-    vec2_t<R> x[2][2];  // x[cbit][tbit]
-    x[0][0] = a[b];
-    x[0][1] = a[b | T];
-    x[1][0] = a[b | C];
-    x[1][1] = a[b | C | T];
-    vec2_t<R> y0 = cmad2<R>(m.m00, x[pol][0], m.m01, x[pol][1]);
-    vec2_t<R> y1 = cmad2<R>(m.m10, x[pol][0], m.m11, x[pol][1]);
-    x[pol][0] = y0;
-    x[pol][1] = y1;
-    uint64_t ib = pol ? (b | C) : b;
-    a[ib] = y0;
-    a[ib | T] = y1;
-#pragma unroll
-    for (int cb = 0; cb < 2; ++cb) {  // target sums over both control halves
-      double ar = x[cb][0].x, ai = x[cb][0].y, br = x[cb][1].x, bi = x[cb][1].y;
-      v[4] += ar * br + ai * bi;
-      v[5] += ar * bi - ai * br;
-      v[6] += ar * ar + ai * ai;
-      v[7] += br * br + bi * bi;
-    }
-#pragma unroll
-    for (int tb = 0; tb < 2; ++tb) {  // control sums over both target halves
-      double ar = x[0][tb].x, ai = x[0][tb].y, br = x[1][tb].x, bi = x[1][tb].y;
-      v[0] += ar * br + ai * bi;
-      v[1] += ar * bi - ai * br;
-      v[2] += ar * ar + ai * ai;
-      v[3] += br * br + bi * bi;
-    }
-  }
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nquads; k += stride)
+    ctrl_bloch_quad<R>(a, insert0(insert0(k, lo), hi), C, T, pol, m, v);
   block_reduce_finish<8>(v, ro);
 }
 
