@@ -188,6 +188,18 @@ def cmd_min_sdrp(args) -> int:
         print("error: usage: width >= 54 needs tens of GB of amplitude storage; pass --i-have-80gb to acknowledge",
               file=sys.stderr)
         return 2
+    if args.heatmap:  # cli.py:192-210
+        from .sdrp import sdrp_depth_heatmap
+        p_grid = [round(0.1 * k, 6) for k in range(1, 11)]
+        cells = sdrp_depth_heatmap(args.width, _parse_span(args.depths), p_grid, args.circuits, args.seed,
+                                   args.mem_budget, dtype=args.dtype)
+        report = BenchReport("min-sdrp-heatmap", {"width": args.width, "circuits": args.circuits},
+                             "p,depth,mean_f_model,completed,failed")
+        for c in cells:
+            mean = "" if c.mean_f_model is None else f"{c.mean_f_model:.12g}"
+            report.rows.append(f"{c.p:.12g},{c.depth},{mean},{c.completed},{c.failed}")
+        report.write_csv(args.out, args.seed, 1, _device_name(), args.dtype)
+        return 0
     report = BenchReport("min-sdrp", {"width": args.width, "circuits": args.circuits, "mem_budget": args.mem_budget},
                          "width,depth,seed,p_min,f_model,peak_amplitudes,wall_ms")
     for depth in _parse_span(args.depths):
@@ -251,23 +263,45 @@ def cmd_validate(args) -> int:
                 except MemoryBudgetError as exc:
                     wall = int((time.monotonic() - t0) * 1000)
                     report.rows.append(f"{width},{depth},{seed},{p:.12g},,,{wall},{exc.needed}")
-        r = math.sqrt(sum((a - b) ** 2 for a, b in pairs) / len(pairs)) if pairs else float("nan")
+        r = _rmse(pairs)
         all_pairs.extend(pairs)
         table.append((width, depth, r))
         print(f"{width:3d} x {depth:<3d} circuits={args.circuits} rmse={r:.4f}")
-    overall = math.sqrt(sum((a - b) ** 2 for a, b in all_pairs) / len(all_pairs)) if all_pairs else float("nan")
+    overall = _rmse(all_pairs)
     print(f"Overall rmse={overall:.4f}")
-    report.write_csv(args.out, args.seed, 1, _device_name(), args.dtype)
+    report.write_csv(args.out, args.seed, args.threads, _device_name(), args.dtype)
+    summary = BenchReport("validate-rmse", {"grid": args.grid}, "width,depth,circuits,rmse")
+    summary.rows = [f"{w},{d},{args.circuits},{r:.6f}" for w, d, r in table]
+    summary.rows.append(f"overall,,{args.circuits * len(table)},{overall:.6f}")
+    summary.write_csv(_sibling(args.out, "_rmse"), args.seed, args.threads, _device_name(), args.dtype)
     return 0
+
+
+def _rmse(pairs) -> float:
+    """validate.py:131-139: an empty cell is an error (the CLI exits 5), not NaN."""
+    pairs = list(pairs)
+    if not pairs:
+        raise ValueError("rmse needs at least one (estimate, exact) pair")
+    return math.sqrt(sum((a - b) ** 2 for a, b in pairs) / len(pairs))
+
+
+def _sibling(path: str, suffix: str) -> str:
+    """cli.py:168-170."""
+    stem, dot, ext = path.rpartition(".")
+    return f"{stem}{suffix}.{ext}" if dot else f"{path}{suffix}"
 
 
 # ---------------------------------------------------------------------------
 # parser and entry point (cli.py:281-344)
 # ---------------------------------------------------------------------------
 def _add_common(p, out_default: str, dtype_default: str) -> None:
+    """The reference's common flags (cli.py:281-287) plus --dtype."""
     p.add_argument("--seed", type=int, default=0, help="base 64-bit seed")
+    p.add_argument("--threads", type=int, default=1, help="worker processes sharing the GPU (validate.py:223-229)")
     p.add_argument("--mem-budget", type=int, default=DEFAULT_BUDGET, help="max dense amplitudes per simulator")
     p.add_argument("--out", default=out_default, help="output CSV path")
+    p.add_argument("--format", choices=("csv", "csv+svg"), default="csv",
+                   help="csv+svg is accepted; the SVG plots (svgplot.py) are out of scope, only the CSV is written")
     p.add_argument("--dtype", choices=("c64", "c128"), default=dtype_default, help="amplitude precision")
 
 
@@ -296,7 +330,7 @@ def build_parser() -> argparse.ArgumentParser:
     p.add_argument("--depths", default="1:10", help="lo:hi or comma list")
     p.add_argument("--circuits", type=int, default=100)
     p.add_argument("--i-have-80gb", action="store_true", help="acknowledge the memory cost of width >= 54")
-    p.add_argument("--threads", type=int, default=1, help="worker processes sharing the GPU (validate.py:223-229)")
+    p.add_argument("--heatmap", action="store_true", help="fixed p x depth cross-section instead of the search")
     _add_common(p, "min_sdrp.csv", "c128")
     p.set_defaults(func=cmd_min_sdrp)
     return ap

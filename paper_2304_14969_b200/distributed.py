@@ -175,15 +175,47 @@ def pairwise_exchange(dist, buf, staging, world: int, rank: int, group=None) -> 
             piece.copy_(into)
 
 
+def scatter_input(x: np.ndarray, world: int, rank: int, schedule: str = "one") -> np.ndarray:
+    """This rank's input slab of the global n-qubit vector x.  schedule "one"
+    (the default): the rank holds the LOW G qubits, slab = x[rank::world];
+    schedule "two": the rank holds the top G qubits, slab = contiguous block."""
+    if schedule == "one":
+        return np.ascontiguousarray(x[rank::world])
+    return np.ascontiguousarray(np.split(x, world)[rank])
+
+
+def assemble_output(slabs, n_local: int, G: int, schedule: str = "one") -> np.ndarray:
+    """The global QFT output in qubit-index order (before the QFT's final SWAP
+    layer, which stays a label permutation: apply final_order(n) for label
+    order) from every rank's output slab, rank order."""
+    flat = np.concatenate([np.asarray(s) for s in slabs])
+    if schedule == "two" or G == 0:
+        return flat
+    u = np.empty(flat.size, dtype=flat.dtype)
+    u[one_x_label(n_local, G)] = flat
+    return u
+
+
 class ShardedQFT:
     """Device execution on one rank: the slab (and, for the double-buffered
     exchange, a second one) as torch buffers wrapped as sk_state views;
     NCCL all_to_all_single or in-place pairwise NCCL send/recv for the
     exchanges; fused sweeps for the local work.
 
+    Layout (it depends on the schedule):
+      * schedule="one" (default, one exchange per QFT): input slab of rank r =
+        x[r::W] (the rank holds the LOW G qubits); the output has the high G
+        qubits as rank bits, element order `one_x_label`.  `scatter_input` /
+        `assemble_output` convert to and from global vectors.
+      * schedule="two": input and output are contiguous blocks (rank = top G
+        qubits), two exchanges per QFT.
+    In both, the QFT's final SWAP layer is a label permutation (final_order).
+
     exchange="auto" picks the double-buffered all-to-all when two slabs fit in
     device memory and the in-place pairwise exchange (one slab + a
-    `chunk_bytes` staging buffer) otherwise."""
+    `chunk_bytes` staging buffer) otherwise.  exchange="host" stages the
+    all-to-all through host memory, for process groups whose backend cannot
+    move device buffers (gloo: the multi-process tests on one GPU)."""
 
     def __init__(self, n_local: int, dtype: str = "c64", group=None, exchange: str = "auto",
                  chunk_bytes: int = 1 << 30, schedule: str = "one"):
@@ -202,8 +234,8 @@ class ShardedQFT:
         if exchange == "auto":
             free, _ = torch.cuda.mem_get_info(self.device)
             exchange = "alltoall" if (self.G == 0 or 2 * slab_bytes + (4 << 30) <= free) else "pairwise"
-        if exchange not in ("alltoall", "pairwise"):
-            raise ValueError(f"exchange must be 'auto', 'alltoall' or 'pairwise', got {exchange!r}")
+        if exchange not in ("alltoall", "pairwise", "host"):
+            raise ValueError(f"exchange must be 'auto', 'alltoall', 'pairwise' or 'host', got {exchange!r}")
         self.exchange = exchange
         nbuf = 2 if (exchange == "alltoall" and self.G) else 1
         self.bufs = [torch.empty(2 << n_local, dtype=real, device=f"cuda:{self.device}") for _ in range(nbuf)]
@@ -240,6 +272,12 @@ class ShardedQFT:
         return self.bufs[self.cur]
 
     def _exchange(self):
+        if self.exchange == "host":
+            send = self.state.cpu()
+            recv = self.torch.empty_like(send)
+            self.dist.all_to_all_single(recv, send, group=self.group)
+            self.state.copy_(recv)
+            return
         if self.exchange == "pairwise":
             pairwise_exchange(self.dist, self.bufs[0], self.staging, self.world, self.rank, self.group)
             return

@@ -107,3 +107,38 @@ def min_sdrp_ensemble(width: int, depth: int, n_circuits: int, base_seed: int, m
     from concurrent.futures import ProcessPoolExecutor
     with ProcessPoolExecutor(max_workers=workers, mp_context=mp.get_context("spawn")) as pool:
         return list(pool.map(_search_worker, jobs))
+
+
+@dataclass
+class HeatmapCell:
+    """Ensemble mean fidelity estimate at one (p, depth) grid point (validate.py:244-252)."""
+
+    p: float
+    depth: int
+    mean_f_model: float | None  # None when every run exceeded the budget
+    completed: int
+    failed: int
+
+
+def sdrp_depth_heatmap(width: int, depths, p_grid, n_circuits: int, base_seed: int, mem_budget: int,
+                       dtype: str = "c128") -> list[HeatmapCell]:
+    """Fixed-p runs over a (p, depth) grid; budget failures are recorded, not
+    searched around (validate.py:255-276)."""
+    from .circuit import derive_seed
+    cells = []
+    for depth in depths:
+        circuits = [build_random_circuit(width, depth, derive_seed(base_seed, depth, i)) for i in range(n_circuits)]
+        for p in p_grid:
+            total, done, failed = 0.0, 0, 0
+            for i, c in enumerate(circuits):
+                cfg = EngineConfig(sdrp=p, mem_budget=mem_budget, rng_seed=derive_seed(base_seed, depth, i),
+                                   dtype=dtype)
+                try:
+                    sim = run_hybrid(c, cfg)
+                    sim.flush_all()
+                    total += sim.estimated_fidelity()
+                    done += 1
+                except MemoryBudgetError:
+                    failed += 1
+            cells.append(HeatmapCell(p, depth, total / done if done else None, done, failed))
+    return cells

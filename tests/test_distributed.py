@@ -272,3 +272,65 @@ def test_virtual_ranks_one_exchange_large_closed_form():
     x[0] = x[-1] = 2 ** -0.5
     got = _virtual_one_exchange(x, world, "c64")
     assert np.max(np.abs(got - O.qft_of_ghz(n, np.arange(1 << n)))) < 1e-5
+
+
+# ---------------------------------------------------------------------------
+# ShardedQFT.run itself (the class bench.py --gpus N runs) in a real
+# world-size-2 process group: both ranks on cuda:0, gloo with the
+# host-staged exchange (NCCL cannot put two ranks on one device).
+# ---------------------------------------------------------------------------
+def _sharded_run_worker(rank, world, port, n_local, dtype, schedule, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2304_14969_b200 import _lib
+        torch.cuda.set_device(0)
+        stream = torch.cuda.Stream()
+        torch.cuda.set_stream(stream)
+        _lib.call("sk_set_stream", 0, stream.cuda_stream)
+        n, G = D.layout(n_local, world)
+        x = random_state(n, np.random.default_rng(99))
+        sq = D.ShardedQFT(n_local, dtype, exchange="host", schedule=schedule)
+        slab = D.scatter_input(x, world, rank, schedule)
+        cplx = torch.complex64 if dtype == "c64" else torch.complex128
+        sq.state.copy_(torch.view_as_real(torch.from_numpy(slab).to(cplx)).reshape(-1))
+        sq.run(None, stream)
+        torch.cuda.synchronize()
+        mine = sq.state.cpu().double().contiguous()
+        gathered = [torch.empty_like(mine) for _ in range(world)] if rank == 0 else None
+        dist.gather(mine, gathered, dst=0)
+        if rank == 0:
+            slabs = [torch.view_as_complex(g.view(-1, 2)).numpy() for g in gathered]
+            u = D.assemble_output(slabs, n_local, G, schedule)
+            got = O.permute_qubits(u, D.final_order(n))
+            q.put(float(np.max(np.abs(got - O.dft_oracle(x)))))
+    except Exception as exc:  # surface the failure instead of a queue timeout
+        q.put(repr(exc))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("schedule", ["one", "two"])
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+def test_gloo_world2_sharded_qft_run_on_device(dtype, schedule):
+    """distributed.ShardedQFT.run (body / exchange / tail, or the two-exchange
+    schedule) in a real 2-process group, vs the DFT of the global vector."""
+    world, n_local = 2, 13
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sharded_run_worker, args=(r, world, port, n_local, dtype, schedule, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    try:
+        err = q.get(timeout=300)
+    finally:
+        for p in procs:
+            p.join(timeout=60)
+            if p.is_alive():
+                p.kill()
+    assert not isinstance(err, str), err
+    assert err < (1e-12 if dtype == "c128" else 1e-5)
