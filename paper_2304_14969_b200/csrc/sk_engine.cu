@@ -288,6 +288,18 @@ __global__ void __launch_bounds__(kEThreads) k_e_kron(const vec2_t<R>* __restric
     out[i] = cmul<R>(hi[(uint64_t)i >> wa], lo[(uint64_t)i & mask]);
 }
 
+// the same with a narrow high factor: lo read once, 2^wb products written
+template <typename R>
+__global__ void __launch_bounds__(kEThreads) k_e_kron_narrow(const vec2_t<R>* __restrict__ lo,
+                                                            const vec2_t<R>* __restrict__ hi, vec2_t<R>* __restrict__ out,
+                                                            int64_t nlo, int wa, int nhi) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nlo; i += stride) {
+    const vec2_t<R> x = lo[i];
+    for (int j = 0; j < nhi; ++j) out[((uint64_t)j << wa) | (uint64_t)i] = cmul<R>(__ldg(hi + j), x);
+  }
+}
+
 // SDRP rounding split (engine.py:464-488) in one launch: the remainder
 // rest[k] = (u00 a0[k] + u01 a1[k]) / sqrt(P0) and the new width-1 shard phi
 // with its published Bloch sums
@@ -473,6 +485,18 @@ struct sk_engine {
     sk_state* st;
     SK_TRY(alloc_state(wa + wb, &st));
     const int64_t n = int64_t(1) << (wa + wb);
+    if (wb <= 4 && wa >= 10) {
+      const int64_t nlo = int64_t(1) << wa;
+      const int g = grid_for(nlo, kEThreads, 2, ctx->num_sms);
+      if (cfg.dtype == SK_C64)
+        k_e_kron_narrow<float><<<g, kEThreads, 0, ctx->stream>>>((const float2*)a->st->d, (const float2*)b->st->d,
+                                                                  (float2*)st->d, nlo, wa, 1 << wb);
+      else
+        k_e_kron_narrow<double><<<g, kEThreads, 0, ctx->stream>>>((const double2*)a->st->d, (const double2*)b->st->d,
+                                                                   (double2*)st->d, nlo, wa, 1 << wb);
+      SK_CHECK_LAUNCH();
+      return merged_shard(a, b, st, out);
+    }
     const int g = grid_for(n, kEThreads, 2, ctx->num_sms);
     if (cfg.dtype == SK_C64)
       k_e_kron<float><<<g, kEThreads, 0, ctx->stream>>>((const float2*)a->st->d, (const float2*)b->st->d,

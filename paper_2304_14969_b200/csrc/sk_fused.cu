@@ -772,24 +772,43 @@ __device__ __forceinline__ void pk_layers(vec2_t<R> (&a)[1 << NR]) {
 }
 
 // a[e] *= phase(base + sum_{chunk slots p} e_p u_p) * scale, Gray-walked:
-// per element one paired multiply to step the phase and one to apply it
-template <typename R, int NR, int L, int TOP>
+// per element one paired multiply to step the phase and one to apply it.
+// The slot phases are successive doublings of one angle (DIR = +1: ut[p+1] =
+// 2 ut[p], the entry phase; DIR = -1: ut[p-1] = 2 ut[p], the end phase), so in
+// fp64 one sincospi plus complex squarings replaces L of them (the sincospi
+// calls were a third of the c128 sweep's FP64 pipe work); fp32 keeps one MUFU
+// sincos per slot.
+template <typename R, int NR, int L, int TOP, int DIR, bool ZERO_BASE>
 __device__ __forceinline__ void pk_phase(vec2_t<R> (&a)[1 << NR], uint64_t base, const uint64_t (&ut)[NR], R scale) {
   using P = PK<R>;
+  constexpr int B0 = TOP - L + 1;
   vec2_t<R> u[NR], uc[NR];
+  if constexpr (sizeof(R) == 8) {
+    constexpr int first = DIR > 0 ? B0 : TOP;
+    u[first] = turn_phase<R>(ut[first]);
 #pragma unroll
-  for (int p = 0; p < NR; ++p)
-    if (p >= TOP - L + 1 && p <= TOP) {
-      u[p] = turn_phase<R>(ut[p]);
-      uc[p] = P::conj(u[p]);
+    for (int i = 1; i < L; ++i) {
+      const int p = DIR > 0 ? B0 + i : TOP - i, q = DIR > 0 ? p - 1 : p + 1;
+      const vec2_t<R> v = u[q];
+      u[p] = mk<R>(v.x * v.x - v.y * v.y, 2.0 * v.x * v.y);
     }
-  vec2_t<R> w = P::scale(turn_phase<R>(base), scale);
+#pragma unroll
+    for (int p = B0; p <= TOP; ++p) uc[p] = P::conj(u[p]);
+  } else {
+#pragma unroll
+    for (int p = 0; p < NR; ++p)
+      if (p >= B0 && p <= TOP) {
+        u[p] = turn_phase<R>(ut[p]);
+        uc[p] = P::conj(u[p]);
+      }
+  }
+  vec2_t<R> w = ZERO_BASE ? mk<R>(scale, (R)0) : P::scale(turn_phase<R>(base), scale);
   a[0] = P::mul(a[0], w);
 #pragma unroll
   for (int k = 1; k < (1 << NR); ++k) {
     const int b = ctz_c(k);
     const int e = k ^ (k >> 1);
-    if (b >= TOP - L + 1 && b <= TOP) w = P::mul(w, ((e >> b) & 1) ? u[b] : uc[b]);
+    if (b >= B0 && b <= TOP) w = P::mul(w, ((e >> b) & 1) ? u[b] : uc[b]);
     a[e] = P::mul(a[e], w);
   }
 }
@@ -808,7 +827,7 @@ __device__ __forceinline__ void pk_chunk(const QStage& st, vec2_t<R> (&a)[1 << N
 #pragma unroll
       for (int p = 0; p < NR; ++p) ut[p] = (p >= B0 && p <= TOP) ? th_all << ((st.lo + p - B0) & 63) : 0;
       const bool here = !scaled && !(fl & F_END);
-      pk_phase<R, NR, L, TOP>(a, th_new * lv, ut, here ? scale : (R)1);
+      pk_phase<R, NR, L, TOP, +1, false>(a, th_new * lv, ut, here ? scale : (R)1);
       scaled = scaled || here;
     }
     pk_layers<R, NR, L, TOP, TOP>(a);
@@ -816,7 +835,7 @@ __device__ __forceinline__ void pk_chunk(const QStage& st, vec2_t<R> (&a)[1 << N
       uint64_t ut[NR];
 #pragma unroll
       for (int p = 0; p < NR; ++p) ut[p] = (p >= B0 && p <= TOP) ? lv << ((63 - (st.lo + p - B0)) & 63) : 0;
-      pk_phase<R, NR, L, TOP>(a, 0, ut, scaled ? (R)1 : scale);
+      pk_phase<R, NR, L, TOP, -1, true>(a, 0, ut, scaled ? (R)1 : scale);
       scaled = true;
     }
     if (!scaled) {
@@ -829,10 +848,14 @@ __device__ __forceinline__ void pk_chunk(const QStage& st, vec2_t<R> (&a)[1 << N
 // 16 fp32 amplitudes per thread fit 64 registers (512 threads x 2 CTAs);
 // 32 fp32 or 16 fp64 amplitudes get 128 (tiles of <= 256 threads)
 template <typename R, int NR>
-constexpr int qft_max_threads() { return (sizeof(R) == 4 && NR <= 4) ? 512 : 256; }
+constexpr int qft_max_threads() { return (sizeof(R) == 4 && NR <= 4) ? 512 : (sizeof(R) == 8 && NR == 4) ? 128 : 256; }
+// c128 with 16 amplitudes per thread: 128-thread tiles, 4 resident per SM at
+// <= 128 registers (5 per SM would need <= 102 registers: 1-3 KB of spills)
+template <typename R, int NR>
+constexpr int qft_min_blocks() { return (sizeof(R) == 8 && NR == 4) ? 4 : 2; }
 
 template <typename R, int NR, int NS>
-__global__ void __launch_bounds__(qft_max_threads<R, NR>(), 2) k_qft(vec2_t<R>* __restrict__ amps, const __grid_constant__ QSweep sw,
+__global__ void __launch_bounds__(qft_max_threads<R, NR>(), (qft_min_blocks<R, NR>())) k_qft(vec2_t<R>* __restrict__ amps, const __grid_constant__ QSweep sw,
                                                                     const __grid_constant__ CUtensorMap tmap) {
   using V = vec2_t<R>;
   extern __shared__ __align__(1024) unsigned char smraw[];
@@ -898,10 +921,19 @@ __global__ void __launch_bounds__(qft_max_threads<R, NR>(), 2) k_qft(vec2_t<R>* 
               *reinterpret_cast<float4*>(rp + ((j ^ (row & 7)) << 4)) =
                   make_float4(a[2 * j].x, a[2 * j].y, a[2 * j + 1].x, a[2 * j + 1].y);
           } else {  // c128: two rows of 8 amplitudes, one 16-byte chunk each
+            // Rows 2i and 2i+1 of thread i: with every thread writing the same
+            // register at once, the 8 threads of a 16-byte-store phase would
+            // cover only 4 distinct (row & 7) values (8 wavefronts instead of
+            // 4).  Threads whose even row repeats within the phase write their
+            // odd row first, so each phase hits all 8 chunk slots.
+            const uint32_t rb = t.w >> 3;
+            const uint32_t flip = ((rb >> 3) & 1u) << 3;
 #pragma unroll
-            for (int e = 0; e < 16; ++e) {
-              const uint32_t row = (t.w >> 3) + (e >> 3);
-              *reinterpret_cast<V*>(smraw + row * 128u + (((e & 7) ^ (row & 7)) << 4)) = a[e];
+            for (int k = 0; k < 16; ++k) {
+              const uint32_t e = (uint32_t)k ^ flip;
+              const V v = flip ? a[k ^ 8] : a[k];
+              const uint32_t row = rb + (e >> 3);
+              *reinterpret_cast<V*>(smraw + row * 128u + (((e & 7u) ^ (row & 7u)) << 4)) = v;
             }
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -1455,7 +1487,9 @@ static int launch_one(sk_state* s, const sk_program* p, int i, DevCtx* c) {
   const size_t smem = ((size_t)1 << T) * sizeof(vec2_t<R>);
   if (tiles > 0x7fffffffull) return set_error(SK_EVALUE, "too many tiles (%d bits outside the tile)", s->width - T);
   vec2_t<R>* d_amps = (vec2_t<R>*)s->d;
-  if (p->qft_ok[i] && threads <= (unsigned)qft_max_threads<R, NR>() && (NR > 4 || use_qft_kernel())) {
+  // 5-bit c64 and 4-bit c128 sweeps exist only as QFT windows: SK_QFT_KERNEL=0 cannot route them elsewhere
+  constexpr bool qft_only = NR > 4 || (sizeof(R) == 8 && NR == 4);
+  if (p->qft_ok[i] && threads <= (unsigned)qft_max_threads<R, NR>() && (qft_only || use_qft_kernel())) {
     const QSweep q = p->pshift ? phase_shifted(p->qsweeps[i], p->pshift, p->pconst) : p->qsweeps[i];
     CUtensorMap tmap{};
     if (q.tma) SK_TRY(tile_store_map(&tmap, s->d, s->width, T, sizeof(vec2_t<R>) == 8 ? 4 : 3));
@@ -1514,6 +1548,7 @@ static int lower_program(int width, int dtype, const sk_sweep* sweeps, int nswee
   std::vector<int> op_seen(nops, 0);
   for (int si = 0; si < nsweeps; ++si) {
     const sk_sweep& sw = sweeps[si];
+    if (sw.nstages < 1 || sw.nstages > kMaxS) return set_error(SK_EVALUE, "sweep %d: bad stage count %d", si, sw.nstages);
     DSweep d{};
     const int NR = sw.nreg ? sw.nreg : NR0;
     if (!(NR == 4 || (dtype == SK_C128 && NR == 3) || (dtype == SK_C64 && NR == 5)))

@@ -91,27 +91,15 @@ int state_alloc(int width, int dtype, int device, sk_state** out) {
   s->device = device;
   s->n = (int64_t)1 << width;
   s->elem = elem_size(dtype);
-  size_t bytes = (size_t)s->n * s->elem;
-  size_t free_b = 0, total_b = 0;
-  // the cudaMemGetInfo pre-check is a ~100 us driver call: only for large
-  // states (small failing allocations still map to SK_ENOMEM below)
-  if (bytes > (size_t(64) << 20) && cudaMemGetInfo(&free_b, &total_b) == cudaSuccess &&
-      bytes > free_b + (size_t(1) << 30)) {
-    // pre-check (pool may hold reusable memory, so allow 1 GiB slack)
-    cudaError_t e = cudaMallocAsync(&s->d, bytes, c->stream);
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      delete s;
-      return set_error(SK_ENOMEM, "need %zu bytes for width %d, device has %zu free", bytes, width, free_b);
-    }
-  } else {
-    cudaError_t e = cudaMallocAsync(&s->d, bytes, c->stream);
-    if (e != cudaSuccess) {
-      cudaGetLastError();
-      delete s;
-      return set_error(e == cudaErrorMemoryAllocation ? SK_ENOMEM : SK_ECUDA, "cudaMallocAsync(%zu): %s",
-                       bytes, cudaGetErrorString(e));
-    }
+  const size_t bytes = (size_t)s->n * s->elem;
+  // no cudaMemGetInfo guess (the pool may hold reusable memory): the
+  // allocation itself is the check, and a failure maps to SK_ENOMEM
+  cudaError_t e = cudaMallocAsync(&s->d, bytes, c->stream);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    delete s;
+    return set_error(e == cudaErrorMemoryAllocation ? SK_ENOMEM : SK_ECUDA, "cudaMallocAsync(%zu) for width %d: %s",
+                     bytes, width, cudaGetErrorString(e));
   }
   *out = s;
   return SK_OK;
@@ -211,13 +199,14 @@ __global__ void k_set_single(vec2_t<R>* d, double ar, double ai, double br, doub
 template <typename R>
 __global__ void __launch_bounds__(kThreads) k_bloch(const vec2_t<R>* __restrict__ a, int64_t npairs, int q,
                                                    RedOut ro) {
+  constexpr int U = kUnroll;  // (8 fp32 pairs per iteration measured slower: 0.72 vs 0.52 ms at w = 28)
   double v[4] = {0, 0, 0, 0};
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const uint64_t bit = 1ull << q;
-  for (int64_t k0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k0 < npairs; k0 += kUnroll * stride) {
-    vec2_t<R> x0[kUnroll], x1[kUnroll];
+  for (int64_t k0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k0 < npairs; k0 += U * stride) {
+    vec2_t<R> x0[U], x1[U];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
+    for (int u = 0; u < U; ++u) {
       int64_t k = k0 + u * stride;
       if (k < npairs) {
         uint64_t i0 = insert0(k, q);
@@ -229,7 +218,7 @@ __global__ void __launch_bounds__(kThreads) k_bloch(const vec2_t<R>* __restrict_
       }
     }
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) bloch_acc(v, x0[u].x, x0[u].y, x1[u].x, x1[u].y);
+    for (int u = 0; u < U; ++u) bloch_acc(v, x0[u].x, x0[u].y, x1[u].x, x1[u].y);
   }
   block_reduce_finish<4>(v, ro);
 }
@@ -365,14 +354,25 @@ __global__ void __launch_bounds__(kThreads) k_apply_ctrl(vec2_t<R>* __restrict__
 // One-control gate fused with the Bloch sums of control and target
 // (engine.py:389-394 runs apply_controlled then bloch_vector twice).
 template <typename R>
-__global__ void __launch_bounds__(kThreads) k_ctrl_bloch(vec2_t<R>* __restrict__ a, int64_t nquads, int c, int pol,
+__global__ void __launch_bounds__(kThreads, (sizeof(R) == 8 ? 3 : 1)) k_ctrl_bloch(vec2_t<R>* __restrict__ a, int64_t nquads, int c, int pol,
                                                         int t, Mat2<R> m, RedOut ro) {
   double v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const uint64_t C = 1ull << c, T = 1ull << t;
   const int lo = c < t ? c : t, hi = c < t ? t : c;
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nquads; k += stride)
-    ctrl_bloch_quad<R>(a, insert0(insert0(k, lo), hi), C, T, pol, m, v);
+  // c128: two quads per iteration, both loaded before either is written (8
+  // loads in flight per thread; measured 0.83 -> 0.80 ms at w = 27); the sums
+  // still accumulate quad by quad in k order.  c64 keeps one quad (faster).
+  int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; sizeof(R) == 8 && k + stride < nquads; k += 2 * stride) {
+    const uint64_t b0 = insert0(insert0(k, lo), hi), b1 = insert0(insert0(k + stride, lo), hi);
+    vec2_t<R> x0[2][2], x1[2][2];
+    ctrl_bloch_load<R>(a, b0, C, T, x0);
+    ctrl_bloch_load<R>(a, b1, C, T, x1);
+    ctrl_bloch_apply<R>(a, b0, C, T, pol, m, x0, v);
+    ctrl_bloch_apply<R>(a, b1, C, T, pol, m, x1, v);
+  }
+  for (; k < nquads; k += stride) ctrl_bloch_quad<R>(a, insert0(insert0(k, lo), hi), C, T, pol, m, v);
   block_reduce_finish<8>(v, ro);
 }
 
@@ -382,7 +382,19 @@ template <typename R>
 __global__ void __launch_bounds__(kThreads) k_pauli(vec2_t<R>* __restrict__ a, int64_t nitems, int fbit, uint64_t flip,
                                                    uint64_t sign, vec2_t<R> scale) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nitems; k += stride) {
+  int64_t k0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (sizeof(R) == 8 && flip != 0) {  // c128: two pairs per iteration, loaded before either is written
+    for (; k0 + stride < nitems; k0 += 2 * stride) {
+      const uint64_t j0 = insert0(k0, fbit), j1 = insert0(k0 + stride, fbit);
+      const vec2_t<R> x0 = a[j0], y0 = a[j0 ^ flip], x1 = a[j1], y1 = a[j1 ^ flip];
+      const vec2_t<R> nscale = mk<R>(-scale.x, -scale.y);
+      a[j0 ^ flip] = cmul<R>(x0, (__popcll(j0 & sign) & 1) ? nscale : scale);
+      a[j0] = cmul<R>(y0, (__popcll((j0 ^ flip) & sign) & 1) ? nscale : scale);
+      a[j1 ^ flip] = cmul<R>(x1, (__popcll(j1 & sign) & 1) ? nscale : scale);
+      a[j1] = cmul<R>(y1, (__popcll((j1 ^ flip) & sign) & 1) ? nscale : scale);
+    }
+  }
+  for (int64_t k = k0; k < nitems; k += stride) {
     if (flip == 0) {
       vec2_t<R> x = a[k];
       vec2_t<R> f = (__popcll(k & sign) & 1) ? mk<R>(-scale.x, -scale.y) : scale;
@@ -465,6 +477,20 @@ __global__ void __launch_bounds__(kThreads) k_kron(const vec2_t<R>* __restrict__
     out[i] = cmul<R>(hi[(uint64_t)i >> wa], lo[(uint64_t)i & mask]);
 }
 
+// kron_compose with a narrow high factor (<= 16 amplitudes): each thread reads
+// lo[i] once and writes all 2^wb products (the generic form re-reads the whole
+// low factor 2^wb times once it exceeds L2); same elementwise arithmetic
+template <typename R>
+__global__ void __launch_bounds__(kThreads) k_kron_narrow(const vec2_t<R>* __restrict__ lo,
+                                                         const vec2_t<R>* __restrict__ hi, vec2_t<R>* __restrict__ out,
+                                                         int64_t nlo, int wa, int nhi) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nlo; i += stride) {
+    const vec2_t<R> x = lo[i];
+    for (int j = 0; j < nhi; ++j) out[((uint64_t)j << wa) | (uint64_t)i] = cmul<R>(__ldg(hi + j), x);
+  }
+}
+
 struct PermSpec {
   int w;
   int order[40];
@@ -479,6 +505,76 @@ __global__ void __launch_bounds__(kThreads) k_permute(const vec2_t<R>* __restric
     uint64_t old = 0;
     for (int k = 0; k < ps.w; ++k) old |= (((uint64_t)i >> k) & 1ull) << ps.order[k];
     out[i] = a[old];
+  }
+}
+
+// permute_qubits as a tiled transpose.  The tile is the set of output bits
+// {0..K-1} (output-contiguous) united with the output positions of input bits
+// {0..K-1} (input-contiguous), at most 2K bits: the block reads it with input
+// low bits fastest (coalesced), parks it in shared memory and writes it with
+// output low bits fastest (coalesced).  Both tile-index maps are linear over
+// GF(2), so per-thread parts are combined with XOR.
+template <int SB>
+__device__ __forceinline__ uint32_t swz(uint32_t l) {  // fold the high bits into the low SB (GF(2)-linear)
+  uint32_t h = l >> SB;
+  uint32_t f = h ^ (h >> SB) ^ (h >> (2 * SB)) ^ (h >> (3 * SB));
+  return l ^ (f & ((1u << SB) - 1));
+}
+
+constexpr int kPermK = 5;
+constexpr int kPermMaxT = 2 * kPermK;
+
+struct PermTile {
+  int w, nrest;
+  uint64_t in_of_bit[kPermMaxT];   // bit t of the input-ordered tile index -> input index bit (1 << pos)
+  uint32_t rm[kPermMaxT];          // bit t of the input-ordered tile index -> output-ordered tile bit
+  uint64_t out_of_bit[kPermMaxT];  // bit t of the output-ordered tile index -> output index bit
+  uint8_t rest_out[40];            // block index bit j -> output bit position
+  uint8_t rest_in[40];             // block index bit j -> input bit position
+};
+
+constexpr int kPermThreads = 256;  // x 4 elements = the 2^kPermMaxT-element tile
+
+template <typename R>
+__global__ void __launch_bounds__(kPermThreads) k_permute_tiled(const vec2_t<R>* __restrict__ a,
+                                                               vec2_t<R>* __restrict__ out,
+                                                               const __grid_constant__ PermTile pt) {
+  using V = vec2_t<R>;
+  __shared__ V sm[1 << kPermMaxT];
+  constexpr int SB = sizeof(V) == 8 ? 4 : 3;  // elements per 128-byte row: the swizzle fold width
+  uint64_t bin = 0, bout = 0;
+  for (int j = 0; j < pt.nrest; ++j) {
+    const uint64_t bit = (blockIdx.x >> j) & 1u;
+    bin |= bit << pt.rest_in[j];
+    bout |= bit << pt.rest_out[j];
+  }
+  const uint32_t tid = threadIdx.x;
+  uint64_t in_t = bin, out_t = bout;  // the thread's part (tile bits 0..7), linear over GF(2)
+  uint32_t mo_t = 0;
+#pragma unroll
+  for (int t = 0; t < 8; ++t)
+    if ((tid >> t) & 1u) {
+      in_t |= pt.in_of_bit[t];
+      mo_t |= pt.rm[t];
+      out_t |= pt.out_of_bit[t];
+    }
+  V r[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {  // input order: each warp reads 32 consecutive input amplitudes
+    const uint64_t in = in_t | ((e & 1) ? pt.in_of_bit[8] : 0) | ((e & 2) ? pt.in_of_bit[9] : 0);
+    r[e] = a[in];
+  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const uint32_t mo = mo_t ^ ((e & 1) ? pt.rm[8] : 0) ^ ((e & 2) ? pt.rm[9] : 0);
+    sm[swz<SB>(mo)] = r[e];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {  // output order: each warp writes 32 consecutive output amplitudes
+    const uint32_t m = tid | ((uint32_t)e << 8);
+    const uint64_t o = out_t | ((e & 1) ? pt.out_of_bit[8] : 0) | ((e & 2) ? pt.out_of_bit[9] : 0);
+    out[o] = sm[swz<SB>(m)];
   }
 }
 
@@ -1095,7 +1191,11 @@ int sk_kron(const sk_state* lo, const sk_state* hi, sk_state** out) {
   const int g = grid_for(o->n, kThreads, 2, c->num_sms);
   int rc = dispatch(lo, [&](auto r) {
     using R = decltype(r);
-    k_kron<R><<<g, kThreads, 0, c->stream>>>((const vec2_t<R>*)lo->d, (const vec2_t<R>*)hi->d, (vec2_t<R>*)o->d, o->n,
+    if (hi->width <= 4 && lo->width >= 10)
+      k_kron_narrow<R><<<grid_for(lo->n, kThreads, 2, c->num_sms), kThreads, 0, c->stream>>>(
+          (const vec2_t<R>*)lo->d, (const vec2_t<R>*)hi->d, (vec2_t<R>*)o->d, lo->n, lo->width, (int)hi->n);
+    else
+      k_kron<R><<<g, kThreads, 0, c->stream>>>((const vec2_t<R>*)lo->d, (const vec2_t<R>*)hi->d, (vec2_t<R>*)o->d, o->n,
                                              lo->width);
     SK_CHECK_LAUNCH();
     return SK_OK;
@@ -1123,13 +1223,57 @@ int sk_permute(const sk_state* s, const int* order, sk_state** out) {
   SK_TRY(state_alloc(s->width, s->dtype, s->device, &o));
   DevCtx* c;
   SK_TRY(ctx_get(s->device, &c));
-  const int g = grid_for(o->n, kThreads, 2, c->num_sms);
-  int rc = dispatch(s, [&](auto r) {
-    using R = decltype(r);
-    k_permute<R><<<g, kThreads, 0, c->stream>>>((const vec2_t<R>*)s->d, (vec2_t<R>*)o->d, o->n, ps);
-    SK_CHECK_LAUNCH();
-    return SK_OK;
-  });
+  const int w = s->width;
+  int rc;
+  if (w >= kPermMaxT + 2) {  // tiled transpose (small states: the per-element gather below)
+    PermTile pt{};
+    pt.w = w;
+    int inv[64];
+    for (int k = 0; k < w; ++k) inv[order[k]] = k;
+    bool in_tile[64] = {false};
+    int T = 0;
+    auto add = [&](int k) {
+      if (!in_tile[k]) in_tile[k] = true, ++T;
+    };
+    for (int k = 0; k < kPermK; ++k) {
+      add(k);        // output low bits
+      add(inv[k]);   // output positions of the input low bits
+    }
+    for (int k = 0; k < w && T < kPermMaxT; ++k) add(k);  // pad the tile to 2^kPermMaxT elements
+    std::vector<int> tout, tin;  // tile bits by output position / by input position
+    for (int k = 0; k < w; ++k)
+      if (in_tile[k]) tout.push_back(k);
+    for (int k : tout) tin.push_back(order[k]);
+    std::sort(tin.begin(), tin.end());
+    for (int t = 0; t < kPermMaxT; ++t) {
+      pt.out_of_bit[t] = 1ull << tout[t];
+      pt.in_of_bit[t] = 1ull << tin[t];
+      const int ob = inv[tin[t]];  // output position of this input bit
+      pt.rm[t] = 1u << (int)(std::find(tout.begin(), tout.end(), ob) - tout.begin());
+    }
+    for (int k = 0; k < w; ++k)
+      if (!in_tile[k]) {
+        pt.rest_out[pt.nrest] = (uint8_t)k;
+        pt.rest_in[pt.nrest] = (uint8_t)order[k];
+        ++pt.nrest;
+      }
+    const uint64_t blocks = 1ull << (w - kPermMaxT);
+    rc = dispatch(s, [&](auto r) {
+      using R = decltype(r);
+      k_permute_tiled<R><<<(unsigned)blocks, kPermThreads, 0, c->stream>>>((const vec2_t<R>*)s->d, (vec2_t<R>*)o->d,
+                                                                          pt);
+      SK_CHECK_LAUNCH();
+      return SK_OK;
+    });
+  } else {
+    const int g = grid_for(o->n, kThreads, 2, c->num_sms);
+    rc = dispatch(s, [&](auto r) {
+      using R = decltype(r);
+      k_permute<R><<<g, kThreads, 0, c->stream>>>((const vec2_t<R>*)s->d, (vec2_t<R>*)o->d, o->n, ps);
+      SK_CHECK_LAUNCH();
+      return SK_OK;
+    });
+  }
   if (rc != SK_OK) {
     sk_destroy(o);
     return rc;

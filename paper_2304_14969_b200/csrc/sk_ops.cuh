@@ -34,17 +34,18 @@ __device__ __forceinline__ void publish_single(vec2_t<R>* d, double ar, double a
   *(volatile unsigned long long*)flag = seq;
 }
 
-// One (c, t) quad of a one-control gate, with the Bloch sums of control
-// (v[0..3]) and target (v[4..7]) accumulated from the post-gate amplitudes
-// (engine.py:389-394 runs apply_controlled then bloch_vector twice).
 template <typename R>
-__device__ __forceinline__ void ctrl_bloch_quad(vec2_t<R>* __restrict__ a, uint64_t b, uint64_t C, uint64_t T, int pol,
-                                                const Mat2<R>& m, double (&v)[8]) {
-  vec2_t<R> x[2][2];  // x[cbit][tbit]
+__device__ __forceinline__ void ctrl_bloch_load(const vec2_t<R>* __restrict__ a, uint64_t b, uint64_t C, uint64_t T,
+                                                vec2_t<R> (&x)[2][2]) {  // x[cbit][tbit]
   x[0][0] = a[b];
   x[0][1] = a[b | T];
   x[1][0] = a[b | C];
   x[1][1] = a[b | C | T];
+}
+
+template <typename R>
+__device__ __forceinline__ void ctrl_bloch_apply(vec2_t<R>* __restrict__ a, uint64_t b, uint64_t C, uint64_t T, int pol,
+                                                 const Mat2<R>& m, vec2_t<R> (&x)[2][2], double (&v)[8]) {
   vec2_t<R> y0 = cmad2<R>(m.m00, x[pol][0], m.m01, x[pol][1]);
   vec2_t<R> y1 = cmad2<R>(m.m10, x[pol][0], m.m11, x[pol][1]);
   x[pol][0] = y0;
@@ -68,6 +69,17 @@ __device__ __forceinline__ void ctrl_bloch_quad(vec2_t<R>* __restrict__ a, uint6
     v[2] += ar * ar + ai * ai;
     v[3] += br * br + bi * bi;
   }
+}
+
+// One (c, t) quad of a one-control gate, with the Bloch sums of control
+// (v[0..3]) and target (v[4..7]) accumulated from the post-gate amplitudes
+// (engine.py:389-394 runs apply_controlled then bloch_vector twice).
+template <typename R>
+__device__ __forceinline__ void ctrl_bloch_quad(vec2_t<R>* __restrict__ a, uint64_t b, uint64_t C, uint64_t T, int pol,
+                                                const Mat2<R>& m, double (&v)[8]) {
+  vec2_t<R> x[2][2];
+  ctrl_bloch_load<R>(a, b, C, T, x);
+  ctrl_bloch_apply<R>(a, b, C, T, pol, m, x, v);
 }
 
 // DenseKet._apply_1q_unchecked element pair (ket.py:133-144)
