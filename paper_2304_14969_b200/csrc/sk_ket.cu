@@ -95,6 +95,15 @@ int state_alloc(int width, int dtype, int device, sk_state** out) {
   // no cudaMemGetInfo guess (the pool may hold reusable memory): the
   // allocation itself is the check, and a failure maps to SK_ENOMEM
   cudaError_t e = cudaMallocAsync(&s->d, bytes, c->stream);
+  if (e == cudaErrorMemoryAllocation) {
+    // the pool keeps freed buffers (release threshold raised in ctx_get); on a
+    // miss, hand them back to the device once and retry before reporting OOM
+    cudaGetLastError();
+    cudaMemPool_t pool;
+    if (cudaStreamSynchronize(c->stream) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess)
+      cudaMemPoolTrimTo(pool, 0);
+    e = cudaMallocAsync(&s->d, bytes, c->stream);
+  }
   if (e != cudaSuccess) {
     cudaGetLastError();
     delete s;
@@ -673,6 +682,11 @@ static int check_qubit(const sk_state* s, int q) {
   return SK_OK;
 }
 
+// pageable complex128 host <-> device state transfers (sk_io.cu)
+int staged_upload(DevCtx* c, sk_state* s, const double* host, int64_t n);
+int staged_download(DevCtx* c, const sk_state* s, double* host, int64_t n);
+constexpr int64_t kStagedMin = int64_t(1) << 18;
+
 }  // namespace sk
 
 using namespace sk;
@@ -798,6 +812,7 @@ int sk_upload(sk_state* s, const double* host, int64_t n) {
   if (n != s->n) return set_error(SK_EVALUE, "need %lld amplitudes, got %lld", (long long)s->n, (long long)n);
   DevCtx* c;
   SK_TRY(ctx_get(s->device, &c));
+  if (n >= kStagedMin) return staged_upload(c, s, host, n);  // sk_io.cu: pinned chunks, parallel host pass
   if (s->dtype == SK_C128) {
     SK_CUDA(cudaMemcpyAsync(s->d, host, (size_t)n * 16, cudaMemcpyHostToDevice, c->stream));
     SK_CUDA(cudaStreamSynchronize(c->stream));
@@ -823,6 +838,10 @@ int sk_download(const sk_state* s, double* host, int64_t n) {
   if (n != s->n) return set_error(SK_EVALUE, "need %lld amplitudes, got %lld", (long long)s->n, (long long)n);
   DevCtx* c;
   SK_TRY(ctx_get(s->device, &c));
+  if (n >= kStagedMin) {
+    SK_CUDA(cudaStreamSynchronize(c->stream));  // the state's pending kernels
+    return staged_download(c, s, host, n);
+  }
   if (s->dtype == SK_C128) {
     SK_CUDA(cudaMemcpyAsync(host, s->d, (size_t)n * 16, cudaMemcpyDeviceToHost, c->stream));
     SK_CUDA(cudaStreamSynchronize(c->stream));

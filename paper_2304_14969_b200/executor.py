@@ -99,7 +99,7 @@ def _run_segment(gates, width, state: DenseKet, phys: list[int], dtype: str, dev
         except ValueError:
             plan = None
     if plan is None:
-        plan = fusion.plan_ops(ops, width, dtype, phys=phys)
+        plan = fusion.plan_ops(fusion.merge_1q(ops), width, dtype, phys=phys)
     Program(plan, device).run(state)
     return phys
 

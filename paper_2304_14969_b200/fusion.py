@@ -114,6 +114,38 @@ def lower(circuit: Circuit, phys: list[int] | None = None):
     return ops, phys
 
 
+def merge_1q(ops: list[Op]) -> list[Op]:
+    """Fold each uncontrolled 1q op into the previous uncontrolled 1q op on the
+    same bit when no op in between touches that bit (they commute with
+    everything else in between): m = m_later @ m_earlier.  In Sycamore-style
+    layers a qubit outside every coupler of a layer carries two consecutive
+    U3s (104 of 600 in random 30x20): one dense 2x2 pass instead of two."""
+    out: list[Op] = []
+    last: dict[int, int] = {}  # bit -> index in out of its open 1q op
+    for op in ops:
+        if op.ctrl_mask == 0 and op.kind in (MAT, DIAG):
+            j = last.get(op.qubit)
+            if j is not None:
+                prev = out[j]
+                a = np.array([[complex(op.m[0], op.m[1]), complex(op.m[2], op.m[3])],
+                              [complex(op.m[4], op.m[5]), complex(op.m[6], op.m[7])]])
+                b = np.array([[complex(prev.m[0], prev.m[1]), complex(prev.m[2], prev.m[3])],
+                              [complex(prev.m[4], prev.m[5]), complex(prev.m[6], prev.m[7])]])
+                m = a @ b
+                diag = m[0, 1] == 0 and m[1, 0] == 0
+                out[j] = Op(DIAG if diag else MAT, op.qubit, _m8(m), src=prev.src)
+                continue
+            last[op.qubit] = len(out)
+            out.append(op)
+            continue
+        sm = op.smask
+        for bit in list(last):
+            if (sm >> bit) & 1:
+                del last[bit]
+        out.append(op)
+    return out
+
+
 def _wrap(a: float) -> float:
     return (a + math.pi) % (2 * math.pi) - math.pi
 
@@ -420,6 +452,8 @@ def plan_circuit(circuit: Circuit, dtype: str = "c64", tile_bits: int | None = N
             return plan_qft(circuit.width, dtype, tile_bits, low_bits, phys, len(circuit.gates), qft_nreg)
         except ValueError:
             pass  # geometry the QFT form cannot pad: fall back to generic sweeps
+    if fuse:
+        ops = merge_1q(ops)
     return plan_ops(ops, circuit.width, dtype, tile_bits, low_bits, phys, len(circuit.gates))
 
 
