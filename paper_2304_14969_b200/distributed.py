@@ -324,3 +324,244 @@ class ShardedQFT:
         elem = 8 if self.dtype == "c64" else 16
         per = (self.world - 1) * ((1 << self.n_local) // self.world) * elem
         return per * (1 if self.schedule == "one" else 2)
+
+
+# ---------------------------------------------------------------------------
+# General sharded circuits ("a non-diagonal gate on a global
+# qubit needs a global<->local bit swap"; the QFT above is its specialisation)
+# ---------------------------------------------------------------------------
+def _is_diag(m) -> bool:
+    return m[0, 1] == 0 and m[1, 0] == 0
+
+
+class ShardedState:
+    """An n-qubit state vector sharded over W = 2^G ranks by G global bits,
+    one process per GPU (torch.distributed: NCCL on the box, gloo with
+    host-staged exchanges in the multi-process tests).
+
+    `layout[label]` is the physical bit of logical qubit `label`: bits below
+    n_local are local index bits of every rank's slab, bit n_local + i is bit
+    i of the rank.  `run(circuit)` executes a gate list:
+
+      * SWAPs are label permutations (engine.py:525-535);
+      * gates on local bits are planned by fusion.py into fused sweeps
+        (k_sweep / k_qft) on this rank's slab;
+      * a control on a global bit is a rank predicate: the gate is dropped on
+        ranks whose bit mismatches and loses the control elsewhere;
+      * a diagonal gate whose target is global is a rank constant: a phase on
+        the slab (or, with local controls, a controlled phase on one of them);
+      * a non-diagonal gate on a global qubit first swaps that global bit with
+        the local bit whose qubit is needed again furthest in the future
+        (Belady): partner ranks (rank ^ 2^i) exchange the half of their slab
+        whose local bit disagrees with their rank bit — one NVLink transfer
+        of half a slab per rank, chunked through a staging buffer.
+    Rank 0 starts in |0...0>."""
+
+    def __init__(self, n: int, dtype: str = "c64", group=None, exchange: str = "auto",
+                 chunk_bytes: int = 1 << 30):
+        import torch
+        import torch.distributed as dist
+
+        self.torch, self.dist, self.group = torch, dist, group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.G = self.world.bit_length() - 1
+        if (1 << self.G) != self.world:
+            raise ValueError(f"world size must be a power of two, got {self.world}")
+        self.n, self.dtype = n, dtype
+        self.n_local = n - self.G
+        if self.n_local < fusion.GEOMETRY[dtype]["nreg"] + 1:
+            raise ValueError(f"need more than {fusion.GEOMETRY[dtype]['nreg']} local qubits, got {self.n_local}")
+        if exchange == "auto":
+            exchange = "nccl" if dist.is_initialized() and dist.get_backend(group) == "nccl" else "host"
+        if exchange not in ("nccl", "host"):
+            raise ValueError(f"exchange must be 'auto', 'nccl' or 'host', got {exchange!r}")
+        self.exchange = exchange
+        self.device = torch.cuda.current_device()
+        self.cplx = torch.complex64 if dtype == "c64" else torch.complex128
+        self.slab = torch.zeros(1 << self.n_local, dtype=self.cplx, device=f"cuda:{self.device}")
+        if self.rank == 0:
+            self.slab[0] = 1.0
+        self.chunk_elems = max(1, chunk_bytes // self.slab.element_size())
+        self.layout = list(range(n))
+        self.exchanges = 0
+        self.exchange_bytes = 0
+        h = C.c_void_p()
+        _lib.call("sk_wrap", self.n_local, _lib.DTYPES[dtype], self.device,
+                  torch.view_as_real(self.slab).data_ptr(), C.byref(h))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and _lib._lib is not None:
+            _lib._lib.sk_destroy(h)
+
+    # ---- planning ------------------------------------------------------------------
+    def _rank_bit(self, phys: int) -> int:
+        return (self.rank >> (phys - self.n_local)) & 1
+
+    def _flush(self, ops: list) -> None:
+        """Run the pending local ops as fused sweeps and empty the list."""
+        if not ops:
+            return
+        plan = fusion.plan_ops(fusion.merge_1q(fusion.fuse_diagonal_runs(list(ops))), self.n_local, self.dtype)
+        ops.clear()
+        from .executor import Program
+        Program(plan, self.device).run_handle(self._h)
+
+    def _victim(self, nd_target, start: int, busy: set[int]) -> int:
+        """Local bit whose qubit's next non-diagonal use lies furthest ahead
+        (nd_target[k] = label acted on non-diagonally by gate k, else -1)."""
+        nxt = {}
+        for k in range(start, len(nd_target)):
+            lab = nd_target[k]
+            if lab >= 0 and lab not in nxt:
+                nxt[lab] = k
+        best, best_at = None, -1
+        for lab in range(self.n):
+            p = self.layout[lab]
+            if p >= self.n_local or p in busy:
+                continue
+            at = nxt.get(lab, len(nd_target) + 1)
+            if at > best_at:
+                best, best_at = p, at
+        return best
+
+    def _swap_bits(self, g: int, loc: int) -> None:
+        """Exchange global bit g with local bit loc (relabel + half-slab transfer)."""
+        i = g - self.n_local
+        b = (self.rank >> i) & 1
+        partner = self.rank ^ (1 << i)
+        # elements whose local bit `loc` disagrees with the rank bit move to the partner
+        view = self.slab.view(-1, 2, 1 << loc)[:, 1 - b, :]
+        flat_rows = view.shape[0]
+        rows_per = max(1, self.chunk_elems // view.shape[1])
+        for r0 in range(0, flat_rows, rows_per):
+            part = view[r0:r0 + rows_per]
+            send = part.contiguous()
+            recv = self.torch.empty_like(send)
+            if self.exchange == "host":
+                s_h, r_h = self.torch.view_as_real(send).cpu(), self.torch.empty(send.shape + (2,), dtype=send.real.dtype)
+                ops = [self.dist.P2POp(self.dist.isend, s_h, partner, self.group),
+                       self.dist.P2POp(self.dist.irecv, r_h, partner, self.group)]
+                for req in self.dist.batch_isend_irecv(ops):
+                    req.wait()
+                recv.copy_(self.torch.view_as_complex(r_h))
+            else:
+                ops = [self.dist.P2POp(self.dist.isend, send, partner, self.group),
+                       self.dist.P2POp(self.dist.irecv, recv, partner, self.group)]
+                for req in self.dist.batch_isend_irecv(ops):
+                    req.wait()
+            part.copy_(recv)
+            self.exchange_bytes += send.numel() * send.element_size()
+        self.exchanges += 1
+        lg = self.layout.index(g)
+        ll = self.layout.index(loc)
+        self.layout[lg], self.layout[ll] = loc, g
+
+    def run(self, circuit) -> None:
+        gates = list(circuit.gates)
+        nd_target = [-1 if g.name in ("swap", "m") or _is_diag(gate_matrix(g.name, g.params)) else g.targets[0]
+                     for g in gates]
+        ops: list[fusion.Op] = []
+        for k, g in enumerate(gates):
+            if g.name == "m":
+                raise ValueError("measurement gates are not supported on sharded states")
+            if g.name == "swap":
+                a, b = g.targets
+                self.layout[a], self.layout[b] = self.layout[b], self.layout[a]
+                continue
+            m = gate_matrix(g.name, g.params)
+            diag = _is_diag(m)
+            if diag and m[0, 0] == 1 and m[1, 1] == 1:
+                continue
+            # controls on global bits are rank predicates
+            live, cmask, cval = True, 0, 0
+            local_ctrls = []
+            for c, pol in zip(g.controls, g.polarity):
+                p = self.layout[c]
+                if p >= self.n_local:
+                    if self._rank_bit(p) != pol:
+                        live = False
+                else:
+                    cmask |= 1 << p
+                    cval |= (1 << p) if pol else 0
+                    local_ctrls.append((p, pol))
+            t = self.layout[g.targets[0]]
+            if t >= self.n_local and not diag:  # bring the target home first
+                self._flush(ops)
+                busy = {self.layout[c] for c in g.controls}
+                self._swap_bits(t, self._victim(nd_target, k + 1, busy))
+                t = self.layout[g.targets[0]]
+                cmask = cval = 0
+                local_ctrls = []
+                live = True
+                for c, pol in zip(g.controls, g.polarity):  # re-resolve: a control may have moved
+                    p = self.layout[c]
+                    if p >= self.n_local:
+                        live = live and self._rank_bit(p) == pol
+                    else:
+                        cmask |= 1 << p
+                        cval |= (1 << p) if pol else 0
+                        local_ctrls.append((p, pol))
+            if not live:
+                continue
+            if t >= self.n_local:  # diagonal on a global target: a rank constant
+                d = m[1, 1] if self._rank_bit(t) else m[0, 0]
+                if local_ctrls:
+                    (p0, pol0), rest = local_ctrls[0], local_ctrls[1:]
+                    dm = np.array([[1, 0], [0, d]] if pol0 else [[d, 0], [0, 1]], dtype=complex)
+                    rm = rv = 0
+                    for p, pol in rest:
+                        rm |= 1 << p
+                        rv |= (1 << p) if pol else 0
+                    ops.append(fusion.Op(fusion.DIAG, p0, fusion._m8(dm), rm, rv))
+                else:
+                    ops.append(fusion.Op(fusion.DIAG, 0, fusion._m8(np.diag([d, d]))))
+                continue
+            ops.append(fusion.Op(fusion.DIAG if diag else fusion.MAT, t, fusion._m8(m), cmask, cval))
+        self._flush(ops)
+
+    # ---- observables (AllReduce of local reductions) ---------------------------------
+    def norm2(self) -> float:
+        out = C.c_double()
+        _lib.call("sk_norm2", self._h, C.byref(out))
+        return self._allreduce(out.value)
+
+    def probability(self, label: int, outcome: int) -> float:
+        p = self.layout[label]
+        if p >= self.n_local:
+            mine = 0.0
+            if self._rank_bit(p) == outcome:
+                out = C.c_double()
+                _lib.call("sk_norm2", self._h, C.byref(out))
+                mine = out.value
+            return self._allreduce(mine)
+        sums = (C.c_double * 4)()
+        _lib.call("sk_bloch_sums", self._h, p, sums)
+        return self._allreduce(sums[3] if outcome else sums[2])
+
+    def _allreduce(self, x: float) -> float:
+        if self.world == 1:
+            return float(x)
+        dev = "cpu" if self.exchange == "host" else f"cuda:{self.device}"
+        t = self.torch.tensor([x], dtype=self.torch.float64, device=dev)
+        self.dist.all_reduce(t, group=self.group)
+        return float(t.item())
+
+    def gather(self) -> np.ndarray | None:
+        """The global state in label order on rank 0 (tests / read-out)."""
+        mine = self.torch.view_as_real(self.slab).cpu().double().contiguous()
+        if self.world == 1:
+            slabs = [mine]
+        else:
+            slabs = [self.torch.empty_like(mine) for _ in range(self.world)] if self.rank == 0 else None
+            self.dist.gather(mine, slabs, dst=0, group=self.group)
+            if self.rank != 0:
+                return None
+        phys_state = np.concatenate([self.torch.view_as_complex(s).numpy() for s in slabs])  # index = rank<<nl | local
+        idx = np.arange(1 << self.n, dtype=np.int64)
+        src = np.zeros_like(idx)
+        for lab in range(self.n):  # label-order index bit lab lives at physical bit layout[lab]
+            src |= ((idx >> lab) & 1) << self.layout[lab]
+        return phys_state[src]

@@ -27,7 +27,7 @@ from paper_2304_14969_b200.circuit import build_ghz, build_qft, build_random_cir
 from paper_2304_14969_b200.executor import compile_circuit  # noqa: E402
 from paper_2304_14969_b200.ket import DenseKet  # noqa: E402
 
-PEAK = 6553.9
+PEAK = json.loads((Path(__file__).resolve().parent.parent / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] if (Path(__file__).resolve().parent.parent / "MEASURED_PEAKS.json").exists() else 6547.2
 stream = torch.cuda.Stream()
 torch.cuda.set_stream(stream)
 _lib.call("sk_set_stream", 0, stream.cuda_stream)
