@@ -233,6 +233,7 @@ typedef struct {
   int32_t dtype;           /* SK_C64 / SK_C128 */
   int32_t device;
   int32_t control_elimination, hx_commutation, label_swap, pauli_coalescing; /* OptFlags */
+  int32_t stabilizer_hybrid; /* OptFlags.stabilizer_hybrid: qubits start as width-1 tableaus (tableau.py) */
 } sk_engine_config;
 
 #define SK_GATE_1Q 0      /* 2x2 on targets[2g] (with controls when ctrl_off[g+1] > ctrl_off[g]) */
@@ -253,11 +254,13 @@ typedef struct {
 #define SK_ENGINE_NSTATS 11
 
 typedef double (*sk_uniform_fn)(void* ctx); /* rng.random() of the caller's PCG64 stream */
+typedef int (*sk_bit_fn)(void* ctx);        /* rng.integers(0, 2) of the same stream (tableau measurements) */
 
 /* HybridState(n, cfg) (engine.py:164-182): n width-1 shards |0>. */
 int sk_engine_create(int n, const sk_engine_config* cfg, sk_engine** out);
 int sk_engine_destroy(sk_engine* e);
 int sk_engine_set_rng(sk_engine* e, sk_uniform_fn fn, void* ctx);
+int sk_engine_set_rng_bits(sk_engine* e, sk_bit_fn fn, void* ctx);
 /* apply_gate for gates [0, ngates) (engine.py:514-573): kind[g], targets[2g..2g+1],
  * controls ctrls[ctrl_off[g] .. ctrl_off[g+1]) with polarities pols[...], matrix mats[8g..8g+7].
  * *done = gates fully applied (the failing gate is not counted). */
@@ -273,14 +276,17 @@ int sk_engine_sdrp_round(sk_engine* e, int label, double p, double* eps_out);
 int sk_engine_stats(const sk_engine* e, int64_t out[SK_ENGINE_NSTATS]);
 int sk_engine_eps(const sk_engine* e, double* out, int64_t cap);
 /* The shards in label order (engine.py _shards_in_label_order): states[i]
- * (borrowed handles, valid until the next engine call), widths[i], and each
- * shard's qubit labels by position, shard after shard, in labels[]. */
-int sk_engine_shards(const sk_engine* e, int cap, sk_state** states, int* widths, int* labels, int* nshards);
+ * (borrowed handles valid until the next engine call; owned[i] = 1 for a
+ * tableau shard's freshly replayed dense ket, which the caller destroys),
+ * widths[i], and each shard's qubit labels by position, shard after shard. */
+int sk_engine_shards(sk_engine* e, int cap, sk_state** states, int* widths, int* labels, int* owned, int* nshards);
 /* load_state (engine.py:768-784): one dense shard, label i = bit i. */
 int sk_engine_load_state(sk_engine* e, const sk_state* s);
-/* measure_all's collapse (engine.py:616-624): every qubit becomes a fresh
- * width-1 shard |bits[label]>. */
-int sk_engine_reset_basis(sk_engine* e, const uint8_t* bits);
+/* measure_all (engine.py:596-626): bits[label] = outcome, dense shards
+ * collapse to fresh width-1 shards, tableaus in place. */
+int sk_engine_measure_all(sk_engine* e, uint8_t* bits);
+/* sample(shots) without collapse (engine.py:628-657): bits[shot * n + label]. */
+int sk_engine_sample(sk_engine* e, int64_t shots, uint8_t* bits);
 
 #ifdef __cplusplus
 }

@@ -40,13 +40,15 @@ class SkSweep(C.Structure):
 class SkEngineConfig(C.Structure):
     _fields_ = [("sdrp", C.c_double), ("separability_tol", C.c_double), ("mem_budget", C.c_int64),
                 ("dtype", C.c_int32), ("device", C.c_int32), ("control_elimination", C.c_int32),
-                ("hx_commutation", C.c_int32), ("label_swap", C.c_int32), ("pauli_coalescing", C.c_int32)]
+                ("hx_commutation", C.c_int32), ("label_swap", C.c_int32), ("pauli_coalescing", C.c_int32),
+                ("stabilizer_hybrid", C.c_int32)]
 
 
 SK_GATE_1Q, SK_GATE_SWAP, SK_GATE_MEASURE = 0, 1, 2
 ENGINE_STATS = ("label_swaps", "kernels", "eliminated_controls", "merges", "splits", "allocs", "amplitude_writes",
                 "dense_total", "peak_amplitudes", "n_eps", "needed")
 UNIFORM_FN = C.CFUNCTYPE(C.c_double, C.c_void_p)
+BIT_FN = C.CFUNCTYPE(C.c_int, C.c_void_p)
 p_engine = C.c_void_p
 i32p = C.POINTER(C.c_int32)
 
@@ -103,6 +105,7 @@ _SIGS = {
     "sk_engine_create": [C.c_int, C.POINTER(SkEngineConfig), C.POINTER(p_engine)],
     "sk_engine_destroy": [p_engine],
     "sk_engine_set_rng": [p_engine, UNIFORM_FN, C.c_void_p],
+    "sk_engine_set_rng_bits": [p_engine, BIT_FN, C.c_void_p],
     "sk_engine_apply": [p_engine, C.c_int, i32p, i32p, i32p, i32p, i32p, dptr, C.POINTER(C.c_int)],
     "sk_engine_measure": [p_engine, C.c_int, C.POINTER(C.c_int)],
     "sk_engine_flush_all": [p_engine],
@@ -111,9 +114,10 @@ _SIGS = {
     "sk_engine_stats": [p_engine, C.POINTER(C.c_int64)],
     "sk_engine_eps": [p_engine, dptr, C.c_int64],
     "sk_engine_shards": [p_engine, C.c_int, C.POINTER(p_state), C.POINTER(C.c_int), C.POINTER(C.c_int),
-                         C.POINTER(C.c_int)],
+                         C.POINTER(C.c_int), C.POINTER(C.c_int)],
     "sk_engine_load_state": [p_engine, p_state],
-    "sk_engine_reset_basis": [p_engine, C.POINTER(C.c_uint8)],
+    "sk_engine_measure_all": [p_engine, C.POINTER(C.c_uint8)],
+    "sk_engine_sample": [p_engine, C.c_int64, C.POINTER(C.c_uint8)],
 }
 _RESTYPES = {"sk_last_error": C.c_char_p}
 

@@ -35,6 +35,7 @@
 
 #include "sk_internal.cuh"
 #include "sk_ops.cuh"
+#include "sk_tableau.h"
 
 namespace {
 
@@ -178,10 +179,12 @@ struct SumsTicket {
 };
 
 struct Shard {
-  sk_state* st = nullptr;
+  sk_state* st = nullptr;                 // dense shards
+  std::unique_ptr<sktab::Tableau> tab;    // stabilizer shards (engine.py Shard kind "stab")
   std::vector<Qubit*> qubits;  // position -> qubit
   SumsTicket sums;             // width-1 shards only
   int width() const { return (int)qubits.size(); }
+  bool stab() const { return (bool)tab; }
 };
 
 constexpr int kRingSlots = 4096;
@@ -324,6 +327,7 @@ __global__ void __launch_bounds__(kEThreads) k_e_round_split(const vec2_t<R>* __
 using namespace sk;
 
 constexpr int kPoolMaxW = 18;   // cache freed shard buffers up to 4 MiB (c128)
+static const float kOneF[2] = {1.0f, 0.0f};
 constexpr size_t kPoolPerW = 32;
 
 struct sk_engine {
@@ -339,6 +343,8 @@ struct sk_engine {
   int64_t needed = 0;  // last budget failure
   sk_uniform_fn ufn = nullptr;
   void* uctx = nullptr;
+  sk_bit_fn bfn = nullptr;  // rng.integers(0, 2): tableau measurements (tableau.py:214)
+  void* bctx = nullptr;
   double* h_ring = nullptr;  // mapped pinned ring of sums slots
   double* d_ring = nullptr;
   int ring_next = 0;
@@ -460,7 +466,17 @@ struct sk_engine {
     return SK_OK;
   }
 
-  int fresh_single(Qubit* q, int bit) {  // engine.py:187-200 (dense branch)
+  int fresh_single(Qubit* q, int bit) {  // engine.py:187-200
+    if (cfg.stabilizer_hybrid) {  // a width-1 tableau, no dense amplitudes
+      Shard* s = new Shard();
+      shards.insert(s);
+      s->tab.reset(new sktab::Tableau(1));
+      if (bit) s->tab->px(0);
+      s->qubits = {q};
+      q->shard = s;
+      q->pos = 0;
+      return SK_OK;
+    }
     SK_TRY(charge(2));
     cd a[2] = {bit ? 0.0 : 1.0, bit ? 1.0 : 0.0};
     sk_state* st;
@@ -478,8 +494,82 @@ struct sk_engine {
     return SK_OK;
   }
 
-  int merge_pair(Shard* a, Shard* b, Shard** out) {  // engine.py:224-243: the wider keeps its positions
-    if (a->width() < b->width()) std::swap(a, b);
+  // exact dense ket of a tableau: replay its log on |0..0> with the device
+  // kernels (tableau.py:258-282)
+  int replay(const sktab::Tableau& t, sk_state** out) {
+    sk_state* st;
+    SK_TRY(alloc_state(t.w, &st));
+    const size_t bytes = (size_t)st->n * st->elem;
+    SK_CUDA(cudaMemsetAsync(st->d, 0, bytes, ctx->stream));
+    const double one[2] = {1.0, 0.0};
+    SK_CUDA(cudaMemcpyAsync(st->d, cfg.dtype == SK_C64 ? (const void*)&kOneF : (const void*)one,
+                            cfg.dtype == SK_C64 ? 8 : 16, cudaMemcpyHostToDevice, ctx->stream));
+    const double s2 = 1.0 / std::sqrt(2.0);
+    const cd e = std::exp(cd(0, 1) * (M_PI / 2));
+    const double H[8] = {s2, 0, s2, 0, s2, 0, -s2, 0};
+    const double S[8] = {1, 0, 0, 0, 0, 0, e.real(), e.imag()};
+    const double X[8] = {0, 0, 1, 0, 1, 0, 0, 0};
+    const double Y[8] = {0, 0, 0, -1, 0, 1, 0, 0};
+    const double Z[8] = {1, 0, 0, 0, 0, 0, -1, 0};
+    int rc = SK_OK;
+    for (const auto& en : t.log) {
+      switch (en.op) {
+        case sktab::L_H: rc = sk_apply_1q(st, en.a, H); break;
+        case sktab::L_S: rc = sk_apply_1q(st, en.a, S); break;
+        case sktab::L_X: rc = sk_apply_1q(st, en.a, X); break;
+        case sktab::L_Y: rc = sk_apply_1q(st, en.a, Y); break;
+        case sktab::L_Z: rc = sk_apply_1q(st, en.a, Z); break;
+        case sktab::L_SWAP: rc = sk_swap_qubits(st, en.a, en.b); break;
+        case sktab::L_CX: rc = sk_apply_controlled(st, 1ull << en.a, 1ull << en.a, en.b, X); break;
+        case sktab::L_M: {
+          double prob;
+          rc = sk_project(st, en.a, en.b, &prob);
+          break;
+        }
+        case sktab::L_GPHASE: rc = sk_scale(st, en.phase.real(), en.phase.imag()); break;
+      }
+      if (rc != SK_OK) {
+        free_state(st);
+        return rc;
+      }
+    }
+    *out = st;
+    return SK_OK;
+  }
+
+  int to_dense(Shard* s) {  // engine.py:216-222
+    if (!s->stab()) return SK_OK;
+    SK_TRY(charge(int64_t(1) << s->width()));
+    sk_state* st;
+    SK_TRY(replay(*s->tab, &st));
+    s->tab.reset();
+    s->st = st;
+    s->sums.kind = kSumsNone;
+    return SK_OK;
+  }
+
+  int merge_pair(Shard* a, Shard* b, Shard** out, bool stab_ok = false) {  // engine.py:224-243
+    if (a->width() < b->width()) std::swap(a, b);  // the wider keeps its positions
+    if (stab_ok && a->stab() && b->stab()) {
+      stats[SK_ENGINE_STAT_MERGES]++;
+      Shard* m = new Shard();
+      shards.insert(m);
+      m->tab.reset(new sktab::Tableau(sktab::merge(*a->tab, *b->tab)));
+      m->qubits = a->qubits;
+      m->qubits.insert(m->qubits.end(), b->qubits.begin(), b->qubits.end());
+      for (int i = 0; i < m->width(); ++i) {
+        m->qubits[i]->shard = m;
+        m->qubits[i]->pos = i;
+      }
+      shards.erase(a);
+      shards.erase(b);
+      delete a;
+      delete b;
+      *out = m;
+      return SK_OK;
+    }
+    SK_TRY(to_dense(a));
+    SK_TRY(to_dense(b));
     const int wa = a->width(), wb = b->width();
     SK_TRY(charge(int64_t(1) << (wa + wb)));
     sk_state* st;
@@ -528,12 +618,13 @@ struct sk_engine {
     return SK_OK;
   }
 
-  int merge_for(const std::vector<Qubit*>& qs, Shard** out) {
+  int merge_for(const std::vector<Qubit*>& qs, Shard** out, bool stab_ok = false) {  // engine.py:245-255
     std::vector<Shard*> list;
     for (Qubit* q : qs)
       if (std::find(list.begin(), list.end(), q->shard) == list.end()) list.push_back(q->shard);
     Shard* m = list[0];
-    for (size_t i = 1; i < list.size(); ++i) SK_TRY(merge_pair(m, list[i], &m));
+    for (size_t i = 1; i < list.size(); ++i) SK_TRY(merge_pair(m, list[i], &m, stab_ok));
+    if (!stab_ok) SK_TRY(to_dense(m));
     *out = m;
     return SK_OK;
   }
@@ -624,15 +715,25 @@ struct sk_engine {
     return true;
   }
 
-  int commit_1q(Qubit* q) {
+  int commit_1q(Qubit* q) {  // engine.py:305-322
     if (!q->has_u) return SK_OK;
     const M2 m = q->u;
     q->has_u = false;
     if (is_identity(m)) return SK_OK;
+    Shard* s = q->shard;
+    if (s->stab()) {  // a Clifford buffer commits into the tableau, anything else converts it
+      std::string word;
+      cd phase;
+      if (sktab::match_clifford_1q(m.a, &word, &phase)) {
+        s->tab->apply_word(word, q->pos);
+        s->tab->append_phase(phase);
+        return SK_OK;
+      }
+      SK_TRY(to_dense(s));
+    }
     if (!unitary(m)) return set_error(SK_EVALUE, "matrix is not unitary within 1e-10");
     double m8[8];
     m_to8(m, m8);
-    Shard* s = q->shard;
     SK_TRY(sk_apply_1q(s->st, q->pos, m8));
     stats[SK_ENGINE_STAT_KERNELS]++;
     stats[SK_ENGINE_STAT_WRITES] += int64_t(1) << s->width();
@@ -695,6 +796,9 @@ struct sk_engine {
     qs.push_back(target);
     double out8[8];
     bool fused = false;
+    bool any_stab = false;
+    for (Qubit* q : qs) any_stab = any_stab || q->shard->stab();
+    if (any_stab) return commit_ctrl_stab(controls, pol, target, m);
     if (controls.size() == 1) SK_TRY(coupler_small(controls[0], pol[0], target, m, out8, &fused));
     if (!fused) {
       for (Qubit* q : qs) SK_TRY(commit_1q(q));
@@ -723,6 +827,54 @@ struct sk_engine {
       bool changed = false;
       SK_TRY(try_factor(qs[i], pre ? pre + 4 * i : nullptr, &changed));
       if (changed) pre = nullptr;  // later operands see a new state: recompute their sums
+    }
+    return SK_OK;
+  }
+
+  // engine.py:367-394 with tableau operands: the coupler stays in the tableau
+  // when it is a single-control Pauli (or identity) and every operand is a
+  // tableau qubit whose 1q buffer is Clifford (engine.py:371-379, 396-403)
+  int commit_ctrl_stab(const std::vector<Qubit*>& controls, const std::vector<int>& pol, Qubit* target, const M2& m) {
+    std::vector<Qubit*> qs = controls;
+    qs.push_back(target);
+    int pauli = -1;
+    bool stab_ok = false;
+    if (cfg.stabilizer_hybrid && controls.size() == 1) {
+      if (max_abs_diff(m, kI) < 1e-12) stab_ok = true;
+      for (int p = 0; p < 3 && !stab_ok; ++p)
+        if (max_abs_diff(m, kPauli[p]) < 1e-12) stab_ok = true;
+    }
+    if (stab_ok) {
+      for (Qubit* q : qs) {
+        std::string word;
+        cd phase;
+        if (!q->shard->stab() || (q->has_u && !sktab::match_clifford_1q(q->u.a, &word, &phase))) stab_ok = false;
+      }
+    }
+    for (Qubit* q : qs) SK_TRY(commit_1q(q));
+    Shard* s;
+    SK_TRY(merge_for(qs, &s, stab_ok));
+    if (s->stab()) {
+      cd ph;
+      pauli = as_pauli(m, &ph);  // engine.py:382 drops the phase (it is 1 here)
+      if (pauli >= 0) s->tab->ctrl_pauli(controls[0]->pos, pol[0], target->pos, pauli);
+    } else {
+      if (!unitary(m)) return set_error(SK_EVALUE, "matrix is not unitary within 1e-10");
+      double m8[8];
+      m_to8(m, m8);
+      uint64_t mask = 0, val = 0;
+      for (size_t i = 0; i < controls.size(); ++i) {
+        mask |= 1ull << controls[i]->pos;
+        if (pol[i]) val |= 1ull << controls[i]->pos;
+      }
+      SK_TRY(sk_apply_controlled(s->st, mask, val, target->pos, m8));
+      stats[SK_ENGINE_STAT_WRITES] += 2 * (int64_t(1) << (s->width() - 1 - (int)controls.size()));
+      s->sums.kind = kSumsNone;
+      stats[SK_ENGINE_STAT_KERNELS]++;
+    }
+    for (Qubit* q : qs) {
+      bool changed;
+      SK_TRY(try_factor(q, nullptr, &changed));
     }
     return SK_OK;
   }
@@ -812,13 +964,22 @@ struct sk_engine {
   int z_eigenstate(Qubit* q, int* z) {
     *z = -1;
     if (!q->pending.empty()) return SK_OK;
-    if (q->shard->width() > 1) return SK_OK;  // entangled-shard scan not worth the pass
     const double tol = cfg.separability_tol;
-    double sums[4];
-    SK_TRY(sums_of(q, sums));
-    const Bloch b = bloch_from_sums(sums);
-    if (epsilon(b) > tol) return SK_OK;
-    double r0[3] = {b.rx, b.ry, b.rz};
+    double r0[3];
+    if (q->shard->stab()) {  // engine.py:418-423
+      int basis, sign;
+      if (!q->shard->tab->deterministic_eigen(q->pos, &basis, &sign)) return SK_OK;
+      r0[0] = basis == 0 ? sign : 0.0;
+      r0[1] = basis == 1 ? sign : 0.0;
+      r0[2] = basis == 2 ? sign : 0.0;
+    } else {
+      if (q->shard->width() > 1) return SK_OK;  // entangled-shard scan not worth the pass
+      double sums[4];
+      SK_TRY(sums_of(q, sums));
+      const Bloch b = bloch_from_sums(sums);
+      if (epsilon(b) > tol) return SK_OK;
+      r0[0] = b.rx, r0[1] = b.ry, r0[2] = b.rz;
+    }
     if (q->has_u) {
       double R[3][3];
       so3(q->u, R);
@@ -911,6 +1072,14 @@ struct sk_engine {
   int try_factor(Qubit* q, const double* given, bool* changed) {
     *changed = false;
     Shard* shard = q->shard;
+    if (shard->stab()) {  // engine.py:444-450: only p = 1 rounds a tableau (a forced measurement)
+      int basis, sign;
+      if (cfg.sdrp >= 1.0 - 1e-12 && shard->width() > 1 && !shard->tab->deterministic_eigen(q->pos, &basis, &sign)) {
+        shard->tab->measure(q->pos, 0, [] { return 0; });
+        eps_push(0.5);
+      }
+      return SK_OK;
+    }
     if (shard->width() < 2) return SK_OK;
     double sums[4];
     if (given)
@@ -952,11 +1121,21 @@ struct sk_engine {
     return commit_ctrl(chs, pol, target, m);
   }
 
+  int tab_measure(Shard* s, int pos, int* outcome) {  // tableau.py:195-221 with the caller's rng
+    if (!bfn) return set_error(SK_EVALUE, "tableau measurement needs the engine rng (sk_engine_set_rng_bits)");
+    *outcome = s->tab->measure(pos, -1, [this] { return bfn(bctx); });
+    return SK_OK;
+  }
+
   int measure_qubit(int label, int* outcome) {  // engine.py:575-594
     Qubit* h = handles[label];
     SK_TRY(flush_pending(h));
     SK_TRY(commit_1q(h));
     Shard* s = h->shard;
+    if (s->stab()) {  // engine.py:580-581
+      SK_TRY(tab_measure(s, h->pos, outcome));
+      return SK_OK;
+    }
     double sums[4];
     SK_TRY(sums_of(h, sums));
     const double p1 = sums[3];
@@ -1048,7 +1227,7 @@ struct sk_engine {
     std::unordered_set<Shard*> seen;
     for (Qubit* h : handles) {
       Shard* s = h->shard;
-      if (!seen.insert(s).second) continue;
+      if (!seen.insert(s).second || s->stab()) continue;
       uint64_t flip = 0, sign = 0;
       int y = 0, count = 0, first_pos = -1, first_p = -1;
       cd scale = 1.0;
@@ -1094,7 +1273,7 @@ struct sk_engine {
     SK_TRY(flush_pending(h));
     SK_TRY(commit_1q(h));
     Shard* s = h->shard;
-    if (s->width() < 2) return set_error(SK_EVALUE, "sdrp_round needs a dense shard of width >= 2");
+    if (s->stab() || s->width() < 2) return set_error(SK_EVALUE, "sdrp_round needs a dense shard of width >= 2");
     double sums[4];
     SK_TRY(sums_of(h, sums));
     const Bloch r = bloch_from_sums(sums);
@@ -1129,6 +1308,7 @@ int sk_engine_create(int n, const sk_engine_config* cfg, sk_engine** out) {
   if (!(cfg->sdrp >= 0.0 && cfg->sdrp <= 1.0)) return set_error(SK_EVALUE, "sdrp must be in [0, 1]");
   if (cfg->mem_budget < 2) return set_error(SK_EVALUE, "mem_budget must be >= 2");
   if (cfg->dtype != SK_C64 && cfg->dtype != SK_C128) return set_error(SK_EVALUE, "bad dtype %d", cfg->dtype);
+  if (cfg->stabilizer_hybrid && n > 64) return set_error(SK_EVALUE, "tableau shards hold at most 64 qubits");
   auto e = std::make_unique<sk_engine>();
   e->n = n;
   e->cfg = *cfg;
@@ -1212,29 +1392,46 @@ int sk_engine_eps(const sk_engine* e, double* out, int64_t cap) {
   return SK_OK;
 }
 
-int sk_engine_shards(const sk_engine* e, int cap, sk_state** states, int* widths, int* labels, int* nshards) {
+int sk_engine_set_rng_bits(sk_engine* e, sk_bit_fn fn, void* ctx) {
+  SK_TRY(check_engine(e));
+  e->bfn = fn;
+  e->bctx = ctx;
+  return SK_OK;
+}
+
+int sk_engine_shards(sk_engine* e, int cap, sk_state** states, int* widths, int* labels, int* owned, int* nshards) {
   SK_TRY(check_engine(e));
   // shards in order of their lowest label (engine.py _shards_in_label_order);
-  // labels[] lists each shard's qubits by position, shard after shard
-  std::vector<int> label_of(e->n);
-  std::unordered_set<const Qubit*> dummy;
-  for (int l = 0; l < e->n; ++l) label_of[l] = 0;
-  std::vector<std::pair<const Qubit*, int>> ql;
+  // labels[] lists each shard's qubits by position, shard after shard; a
+  // tableau shard is handed out as a fresh dense ket (owned[i] = 1, the
+  // caller destroys it; engine.py:712-717: wider than 28 qubits is a budget error)
   std::vector<int> lab(e->own.size());
-  for (int l = 0; l < e->n; ++l) {
-    const Qubit* q = e->handles[l];
+  for (int l = 0; l < e->n; ++l)
     for (size_t i = 0; i < e->own.size(); ++i)
-      if (e->own[i].get() == q) lab[i] = l;
-  }
-  std::vector<const Shard*> order;
+      if (e->own[i].get() == e->handles[l]) lab[i] = l;
+  std::vector<Shard*> order;
   for (int l = 0; l < e->n; ++l) {
-    const Shard* s = e->handles[l]->shard;
+    Shard* s = e->handles[l]->shard;
     if (std::find(order.begin(), order.end(), s) == order.end()) order.push_back(s);
   }
   if ((int)order.size() > cap) return set_error(SK_EVALUE, "need room for %d shards", (int)order.size());
   int k = 0;
   for (size_t i = 0; i < order.size(); ++i) {
-    states[i] = order[i]->st;
+    owned[i] = 0;
+    if (order[i]->stab()) {
+      if (order[i]->width() > 28) {
+        e->needed = int64_t(1) << order[i]->width();
+        for (size_t j = 0; j < i; ++j)
+          if (owned[j]) sk_destroy(states[j]);
+        return set_error(SK_EBUDGET, "needs %lld dense amplitudes", (long long)e->needed);
+      }
+      sk_state* st;
+      SK_TRY(e->replay(*order[i]->tab, &st));
+      states[i] = st;
+      owned[i] = 1;
+    } else {
+      states[i] = order[i]->st;
+    }
     widths[i] = order[i]->width();
     for (const Qubit* q : order[i]->qubits) {
       for (size_t j = 0; j < e->own.size(); ++j)
@@ -1257,7 +1454,8 @@ int sk_engine_load_state(sk_engine* e, const sk_state* s) {  // engine.py:768-78
   }
   for (PendingOp* op : ops) delete op;
   int64_t total = 0;
-  for (Shard* sh : e->shards) total += int64_t(1) << sh->width();
+  for (Shard* sh : e->shards)
+    if (!sh->stab()) total += int64_t(1) << sh->width();  // engine.py:774-777: only dense amplitudes are charged
   SK_TRY(e->release(total));
   SK_TRY(e->charge(int64_t(1) << s->width));
   sk_state* copy;
@@ -1280,14 +1478,85 @@ int sk_engine_load_state(sk_engine* e, const sk_state* s) {  // engine.py:768-78
   return SK_OK;
 }
 
-int sk_engine_reset_basis(sk_engine* e, const uint8_t* bits) {  // measure_all collapse (engine.py:596-626)
+int sk_engine_measure_all(sk_engine* e, uint8_t* bits) {  // engine.py:596-626
   SK_TRY(check_engine(e));
-  std::vector<Shard*> old(e->shards.begin(), e->shards.end());
-  for (Shard* sh : old) {
-    SK_TRY(e->release(int64_t(1) << sh->width()));
-    e->drop_shard(sh);
+  SK_TRY(e->flush_all());
+  std::vector<Shard*> order;
+  for (int l = 0; l < e->n; ++l) {
+    Shard* s = e->handles[l]->shard;
+    if (std::find(order.begin(), order.end(), s) == order.end()) order.push_back(s);
   }
-  for (int l = 0; l < e->n; ++l) SK_TRY(e->fresh_single(e->handles[l], bits[l] ? 1 : 0));
+  std::vector<int> outcome_of(e->own.size());
+  auto idx_of = [e](const Qubit* q) {
+    for (size_t j = 0; j < e->own.size(); ++j)
+      if (e->own[j].get() == q) return (int)j;
+    return -1;
+  };
+  for (Shard* s : order) {
+    if (s->stab()) {  // the tableau collapses in place
+      for (int pos = 0; pos < s->width(); ++pos) {
+        int o;
+        SK_TRY(e->tab_measure(s, pos, &o));
+        outcome_of[idx_of(s->qubits[pos])] = o;
+      }
+      continue;
+    }
+    if (!e->ufn) return set_error(SK_EVALUE, "measure_all needs the engine rng");
+    const double u = e->ufn(e->uctx);  // == rng.choice(size, p=|a|^2): one uniform
+    int64_t idx;
+    SK_TRY(sk_sample(s->st, &u, 1, &idx));
+    std::vector<Qubit*> members = s->qubits;
+    SK_TRY(e->release(int64_t(1) << s->width()));  // before charging the singles
+    e->drop_shard(s);
+    for (int pos = 0; pos < (int)members.size(); ++pos) {
+      const int bit = (int)((idx >> pos) & 1);
+      outcome_of[idx_of(members[pos])] = bit;
+      SK_TRY(e->fresh_single(members[pos], bit));
+    }
+  }
+  for (int l = 0; l < e->n; ++l) bits[l] = (uint8_t)outcome_of[idx_of(e->handles[l])];
+  return SK_OK;
+}
+
+int sk_engine_sample(sk_engine* e, int64_t shots, uint8_t* bits) {  // engine.py:628-657, bits[shot * n + label]
+  SK_TRY(check_engine(e));
+  if (shots < 0) return set_error(SK_EVALUE, "negative shot count");
+  SK_TRY(e->flush_all());
+  std::vector<Shard*> order;
+  for (int l = 0; l < e->n; ++l) {
+    Shard* s = e->handles[l]->shard;
+    if (std::find(order.begin(), order.end(), s) == order.end()) order.push_back(s);
+  }
+  std::vector<int> label_of(e->own.size(), -1);
+  for (int l = 0; l < e->n; ++l)
+    for (size_t j = 0; j < e->own.size(); ++j)
+      if (e->own[j].get() == e->handles[l]) label_of[j] = l;
+  auto lab = [&](const Qubit* q) {
+    for (size_t j = 0; j < e->own.size(); ++j)
+      if (e->own[j].get() == q) return label_of[j];
+    return -1;
+  };
+  for (Shard* s : order) {
+    if (s->stab()) {  // a fresh tableau copy per shot, every qubit measured in order
+      for (int64_t k = 0; k < shots; ++k) {
+        sktab::Tableau t = *s->tab;
+        for (int pos = 0; pos < s->width(); ++pos) {
+          if (!e->bfn) return set_error(SK_EVALUE, "tableau sampling needs the engine rng");
+          bits[k * e->n + lab(s->qubits[pos])] = (uint8_t)t.measure(pos, -1, [e] { return e->bfn(e->bctx); });
+        }
+      }
+      continue;
+    }
+    if (!e->ufn) return set_error(SK_EVALUE, "sampling needs the engine rng");
+    std::vector<double> u(shots);
+    for (auto& v : u) v = e->ufn(e->uctx);  // rng.choice(size=shots): shots uniforms in order
+    std::vector<int64_t> idx(shots);
+    SK_TRY(sk_sample(s->st, u.data(), shots, idx.data()));
+    for (int pos = 0; pos < s->width(); ++pos) {
+      const int l = lab(s->qubits[pos]);
+      for (int64_t k = 0; k < shots; ++k) bits[k * e->n + l] = (uint8_t)((idx[k] >> pos) & 1);
+    }
+  }
   return SK_OK;
 }
 

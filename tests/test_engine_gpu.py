@@ -5,6 +5,8 @@ kernel/merge/split counts, final amplitudes, measurement outcomes and
 samples (same PCG64 draws).  Needs a GPU."""
 from __future__ import annotations
 
+import math
+
 import numpy as np
 import pytest
 
@@ -53,8 +55,7 @@ def test_engine_runs_match_reference(eg):
         np.testing.assert_allclose(sim.eps_record, want, atol=1e-9, err_msg=key)
         assert abs(sim.estimated_fidelity() - float(eg[f"{key}/fmodel"])) < 1e-9, key
         assert sim.peak_amplitudes == int(eg[f"{key}/peak"]), key
-        if not key.endswith("_default"):  # the tableau path counts differently
-            assert [sim.stats[s] for s in STATS] == [int(v) for v in eg[f"{key}/stats"]], key
+        assert [sim.stats[s] for s in STATS] == [int(v) for v in eg[f"{key}/stats"]], key  # incl. tableau runs
         got = sim.full_ket().amps
         assert np.max(np.abs(got - eg[f"{key}/ket"])) < 1e-10, key
 
@@ -100,3 +101,50 @@ def test_sdrp_round_api_and_errors():
     sim.flush_all()
     eps = sim.sdrp_round(0, p=1.0)  # Bell pair: eps = 0.5 <= p/2
     assert abs(eps - 0.5) < 1e-12 and abs(sim.estimated_fidelity() - 0.5) < 1e-12
+
+
+# ---------------------------------------------------------------------------
+# tableau shards (OptFlags.stabilizer_hybrid, the default): Clifford-heavy
+# circuits from oracle/gen_golden_tableau.py, run by the reference engine
+# ---------------------------------------------------------------------------
+def _decode(w, enc):
+    from paper_2304_14969_b200.circuit import Gate
+    names = ["h", "x", "y", "z", "rz", "p", "u3", "swap", "m"]
+    gates = []
+    for row in enc:
+        name = names[int(row[0])]
+        if name == "swap":
+            gates.append(Gate("swap", (int(row[1]), int(row[2]))))
+        elif name == "m":
+            gates.append(Gate("m", (int(row[1]),)))
+        else:
+            params = ()
+            if name == "p":
+                params = (float(row[5]),)
+            elif name == "u3":
+                params = (float(row[5]), float(row[6]), math.pi)
+            if row[3] >= 0:
+                gates.append(Gate(name, (int(row[1]),), params, controls=(int(row[3]),), polarity=(int(row[4]),)))
+            else:
+                gates.append(Gate(name, (int(row[1]),), params))
+    return Circuit(w, tuple(gates))
+
+
+def test_tableau_shards_match_reference(golden):
+    tg = golden("tableau")
+    cases = sorted({k.split("/")[1] for k in tg.files if k.startswith("t/")})
+    assert len(cases) == 15
+    for name in cases:
+        key = f"t/{name}"
+        w, seed = (int(v) for v in tg[f"{key}/spec"])
+        c = _decode(w, tg[f"{key}/gates"])
+        sim = HybridState(w, EngineConfig(sdrp=float(tg[f"{key}/p"]), rng_seed=seed, mem_budget=1 << 16))
+        sim.apply_circuit(c)
+        np.testing.assert_allclose(sim.eps_record, tg[f"{key}/eps"], atol=1e-9, err_msg=name)
+        assert [sim.stats[s] for s in STATS] == [int(v) for v in tg[f"{key}/stats"]], name
+        assert sim.peak_amplitudes == int(tg[f"{key}/peak"]), name
+        assert np.max(np.abs(sim.full_ket().amps - tg[f"{key}/ket"])) < 1e-10, name
+        samples = np.array([int(s[::-1], 2) for s in sim.sample(64)])
+        assert np.array_equal(samples, tg[f"{key}/samples"]), name
+        assert int(sim.measure_all()[::-1], 2) == int(tg[f"{key}/measure_all"][0]), name
+        assert np.max(np.abs(sim.full_ket().amps - tg[f"{key}/ket_after"])) < 1e-10, name
