@@ -541,6 +541,17 @@ struct sk_engine {
     if (!s->stab()) return SK_OK;
     SK_TRY(charge(int64_t(1) << s->width()));
     sk_state* st;
+    if (s->width() == 1 && s->tab->log.empty()) {  // an untouched qubit: |0>, sums exact
+      double h[4] = {1.0, 0.0, 0.0, 0.0};
+      SK_TRY(sk_create_from(1, cfg.dtype, cfg.device, h, &st));
+      stats[SK_ENGINE_STAT_ALLOCS]++;
+      s->tab.reset();
+      s->st = st;
+      s->sums.kind = kSumsHost;
+      s->sums.v[0] = s->sums.v[1] = s->sums.v[3] = 0.0;
+      s->sums.v[2] = 1.0;
+      return SK_OK;
+    }
     SK_TRY(replay(*s->tab, &st));
     s->tab.reset();
     s->st = st;
@@ -798,7 +809,23 @@ struct sk_engine {
     bool fused = false;
     bool any_stab = false;
     for (Qubit* q : qs) any_stab = any_stab || q->shard->stab();
-    if (any_stab) return commit_ctrl_stab(controls, pol, target, m);
+    if (any_stab) {
+      // The fused path below serves tableau operands whose own 1q buffer is
+      // non-Clifford (every qubit of the random-circuit workloads): the
+      // reference's commit_1q converts exactly those shards, in operand order
+      // (engine.py:318-321), before the merge — so convert them here the same
+      // way.  Anything else (a tableau coupler, or a conversion the merge would
+      // order by width) takes the general path.
+      bool fast = controls.size() == 1 && !stab_coupler_ok(controls, target, m);
+      for (Qubit* q : qs) {
+        std::string word;
+        cd phase;
+        if (q->shard->stab() && !(q->has_u && !is_identity(q->u) && !sktab::match_clifford_1q(q->u.a, &word, &phase)))
+          fast = false;
+      }
+      if (!fast) return commit_ctrl_stab(controls, pol, target, m);
+      for (Qubit* q : qs) SK_TRY(to_dense(q->shard));
+    }
     if (controls.size() == 1) SK_TRY(coupler_small(controls[0], pol[0], target, m, out8, &fused));
     if (!fused) {
       for (Qubit* q : qs) SK_TRY(commit_1q(q));
@@ -831,6 +858,21 @@ struct sk_engine {
     return SK_OK;
   }
 
+  // engine.py:371-379, 396-403: the coupler can stay in the tableau (a
+  // single-control Pauli or identity on tableau operands whose 1q buffers are Clifford)
+  bool stab_coupler_ok(const std::vector<Qubit*>& controls, Qubit* target, const M2& m) const {
+    if (!cfg.stabilizer_hybrid || controls.size() != 1) return false;
+    bool ok = max_abs_diff(m, kI) < 1e-12;
+    for (int p = 0; p < 3 && !ok; ++p) ok = max_abs_diff(m, kPauli[p]) < 1e-12;
+    if (!ok) return false;
+    for (Qubit* q : {controls[0], target}) {
+      std::string word;
+      cd phase;
+      if (!q->shard->stab() || (q->has_u && !sktab::match_clifford_1q(q->u.a, &word, &phase))) return false;
+    }
+    return true;
+  }
+
   // engine.py:367-394 with tableau operands: the coupler stays in the tableau
   // when it is a single-control Pauli (or identity) and every operand is a
   // tableau qubit whose 1q buffer is Clifford (engine.py:371-379, 396-403)
@@ -838,19 +880,7 @@ struct sk_engine {
     std::vector<Qubit*> qs = controls;
     qs.push_back(target);
     int pauli = -1;
-    bool stab_ok = false;
-    if (cfg.stabilizer_hybrid && controls.size() == 1) {
-      if (max_abs_diff(m, kI) < 1e-12) stab_ok = true;
-      for (int p = 0; p < 3 && !stab_ok; ++p)
-        if (max_abs_diff(m, kPauli[p]) < 1e-12) stab_ok = true;
-    }
-    if (stab_ok) {
-      for (Qubit* q : qs) {
-        std::string word;
-        cd phase;
-        if (!q->shard->stab() || (q->has_u && !sktab::match_clifford_1q(q->u.a, &word, &phase))) stab_ok = false;
-      }
-    }
+    const bool stab_ok = stab_coupler_ok(controls, target, m);
     for (Qubit* q : qs) SK_TRY(commit_1q(q));
     Shard* s;
     SK_TRY(merge_for(qs, &s, stab_ok));
