@@ -212,6 +212,47 @@ __global__ void __launch_bounds__(kThreads) k_bloch(const vec2_t<R>* __restrict_
   double v[4] = {0, 0, 0, 0};
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const uint64_t bit = 1ull << q;
+  if constexpr (sizeof(R) == 4) {
+    if (npairs >= (int64_t(1) << 12)) {
+      // c64, large: two neighbouring pairs per 16-byte load (pairs 2k, 2k+1
+      // share a float4 in each half; for q = 0 a pair is itself one float4),
+      // so each thread keeps twice the bytes in flight per load instruction
+      const float4* a4 = reinterpret_cast<const float4*>(a);
+      const int64_t nq = npairs >> 1;
+      for (int64_t k0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k0 < nq; k0 += U * stride) {
+        float4 x0[U], x1[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t k = k0 + u * stride;
+          if (k < nq) {
+            if (q == 0) {
+              x0[u] = a4[2 * k];
+              x1[u] = a4[2 * k + 1];
+            } else {
+              const uint64_t i0 = insert0(2 * k, q);
+              x0[u] = a4[i0 >> 1];
+              x1[u] = a4[(i0 | bit) >> 1];
+            }
+          } else {
+            x0[u] = make_float4(0, 0, 0, 0);
+            x1[u] = make_float4(0, 0, 0, 0);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (q == 0) {  // x0 = (a0, a1) of pair 2k, x1 = pair 2k+1
+            bloch_acc(v, x0[u].x, x0[u].y, x0[u].z, x0[u].w);
+            bloch_acc(v, x1[u].x, x1[u].y, x1[u].z, x1[u].w);
+          } else {  // x0 = a0 of pairs 2k, 2k+1; x1 = their a1
+            bloch_acc(v, x0[u].x, x0[u].y, x1[u].x, x1[u].y);
+            bloch_acc(v, x0[u].z, x0[u].w, x1[u].z, x1[u].w);
+          }
+        }
+      }
+      block_reduce_finish<4>(v, ro);
+      return;
+    }
+  }
   for (int64_t k0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k0 < npairs; k0 += U * stride) {
     vec2_t<R> x0[U], x1[U];
 #pragma unroll
@@ -363,7 +404,7 @@ __global__ void __launch_bounds__(kThreads) k_apply_ctrl(vec2_t<R>* __restrict__
 // One-control gate fused with the Bloch sums of control and target
 // (engine.py:389-394 runs apply_controlled then bloch_vector twice).
 template <typename R>
-__global__ void __launch_bounds__(kThreads, (sizeof(R) == 8 ? 3 : 1)) k_ctrl_bloch(vec2_t<R>* __restrict__ a, int64_t nquads, int c, int pol,
+__global__ void __launch_bounds__(kThreads, (sizeof(R) == 8 ? 3 : 4)) k_ctrl_bloch(vec2_t<R>* __restrict__ a, int64_t nquads, int c, int pol,
                                                         int t, Mat2<R> m, RedOut ro) {
   double v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -531,7 +572,7 @@ __device__ __forceinline__ uint32_t swz(uint32_t l) {  // fold the high bits int
 }
 
 constexpr int kPermK = 5;
-constexpr int kPermMaxT = 2 * kPermK;
+constexpr int kPermMaxT = 2 * kPermK + 1;  // tile bits: 10 (c128, 4 elements per thread) or 11 (c64, 8)
 
 struct PermTile {
   int w, nrest;
@@ -542,22 +583,33 @@ struct PermTile {
   uint8_t rest_in[40];             // block index bit j -> input bit position
 };
 
-constexpr int kPermThreads = 256;  // x 4 elements = the 2^kPermMaxT-element tile
+constexpr int kPermThreads = 256;
+
+// tile = 2^(8 + EB) elements: EB = 2 (c128) or 3 (c64), i.e. 64 bytes per
+// thread either way
+template <typename R>
+constexpr int perm_eb() { return sizeof(R) == 4 ? 3 : 2; }
 
 template <typename R>
 __global__ void __launch_bounds__(kPermThreads) k_permute_tiled(const vec2_t<R>* __restrict__ a,
                                                                vec2_t<R>* __restrict__ out,
                                                                const __grid_constant__ PermTile pt) {
   using V = vec2_t<R>;
-  __shared__ V sm[1 << kPermMaxT];
+  constexpr int EB = perm_eb<R>(), E = 1 << EB;
+  __shared__ V sm[kPermThreads * E];
   constexpr int SB = sizeof(V) == 8 ? 4 : 3;  // elements per 128-byte row: the swizzle fold width
+  // block base: lane j deposits block-index bit j, a warp OR-reduction combines them
+  const uint32_t tid = threadIdx.x, lane = tid & 31;
   uint64_t bin = 0, bout = 0;
-  for (int j = 0; j < pt.nrest; ++j) {
+  for (int j = lane; j < pt.nrest; j += 32) {
     const uint64_t bit = (blockIdx.x >> j) & 1u;
     bin |= bit << pt.rest_in[j];
     bout |= bit << pt.rest_out[j];
   }
-  const uint32_t tid = threadIdx.x;
+  bin = ((uint64_t)__reduce_or_sync(0xffffffffu, (uint32_t)(bin >> 32)) << 32) |
+        __reduce_or_sync(0xffffffffu, (uint32_t)bin);
+  bout = ((uint64_t)__reduce_or_sync(0xffffffffu, (uint32_t)(bout >> 32)) << 32) |
+         __reduce_or_sync(0xffffffffu, (uint32_t)bout);
   uint64_t in_t = bin, out_t = bout;  // the thread's part (tile bits 0..7), linear over GF(2)
   uint32_t mo_t = 0;
 #pragma unroll
@@ -567,22 +619,31 @@ __global__ void __launch_bounds__(kPermThreads) k_permute_tiled(const vec2_t<R>*
       mo_t |= pt.rm[t];
       out_t |= pt.out_of_bit[t];
     }
-  V r[4];
+  V r[E];
 #pragma unroll
-  for (int e = 0; e < 4; ++e) {  // input order: each warp reads 32 consecutive input amplitudes
-    const uint64_t in = in_t | ((e & 1) ? pt.in_of_bit[8] : 0) | ((e & 2) ? pt.in_of_bit[9] : 0);
+  for (int e = 0; e < E; ++e) {  // input order: each warp reads 32 consecutive input amplitudes
+    uint64_t in = in_t;
+#pragma unroll
+    for (int b = 0; b < EB; ++b)
+      if ((e >> b) & 1) in |= pt.in_of_bit[8 + b];
     r[e] = a[in];
   }
 #pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    const uint32_t mo = mo_t ^ ((e & 1) ? pt.rm[8] : 0) ^ ((e & 2) ? pt.rm[9] : 0);
+  for (int e = 0; e < E; ++e) {
+    uint32_t mo = mo_t;
+#pragma unroll
+    for (int b = 0; b < EB; ++b)
+      if ((e >> b) & 1) mo ^= pt.rm[8 + b];
     sm[swz<SB>(mo)] = r[e];
   }
   __syncthreads();
 #pragma unroll
-  for (int e = 0; e < 4; ++e) {  // output order: each warp writes 32 consecutive output amplitudes
+  for (int e = 0; e < E; ++e) {  // output order: each warp writes 32 consecutive output amplitudes
     const uint32_t m = tid | ((uint32_t)e << 8);
-    const uint64_t o = out_t | ((e & 1) ? pt.out_of_bit[8] : 0) | ((e & 2) ? pt.out_of_bit[9] : 0);
+    uint64_t o = out_t;
+#pragma unroll
+    for (int b = 0; b < EB; ++b)
+      if ((e >> b) & 1) o |= pt.out_of_bit[8 + b];
     out[o] = sm[swz<SB>(m)];
   }
 }
@@ -1244,7 +1305,8 @@ int sk_permute(const sk_state* s, const int* order, sk_state** out) {
   SK_TRY(ctx_get(s->device, &c));
   const int w = s->width;
   int rc;
-  if (w >= kPermMaxT + 2) {  // tiled transpose (small states: the per-element gather below)
+  const int TB = 8 + (s->dtype == SK_C64 ? 3 : 2);  // tile bits (perm_eb)
+  if (w >= TB + 2) {  // tiled transpose (small states: the per-element gather below)
     PermTile pt{};
     pt.w = w;
     int inv[64];
@@ -1258,13 +1320,13 @@ int sk_permute(const sk_state* s, const int* order, sk_state** out) {
       add(k);        // output low bits
       add(inv[k]);   // output positions of the input low bits
     }
-    for (int k = 0; k < w && T < kPermMaxT; ++k) add(k);  // pad the tile to 2^kPermMaxT elements
+    for (int k = 0; k < w && T < TB; ++k) add(k);  // pad the tile to 2^TB elements
     std::vector<int> tout, tin;  // tile bits by output position / by input position
     for (int k = 0; k < w; ++k)
       if (in_tile[k]) tout.push_back(k);
     for (int k : tout) tin.push_back(order[k]);
     std::sort(tin.begin(), tin.end());
-    for (int t = 0; t < kPermMaxT; ++t) {
+    for (int t = 0; t < TB; ++t) {
       pt.out_of_bit[t] = 1ull << tout[t];
       pt.in_of_bit[t] = 1ull << tin[t];
       const int ob = inv[tin[t]];  // output position of this input bit
@@ -1276,7 +1338,7 @@ int sk_permute(const sk_state* s, const int* order, sk_state** out) {
         pt.rest_in[pt.nrest] = (uint8_t)order[k];
         ++pt.nrest;
       }
-    const uint64_t blocks = 1ull << (w - kPermMaxT);
+    const uint64_t blocks = 1ull << (w - TB);
     rc = dispatch(s, [&](auto r) {
       using R = decltype(r);
       k_permute_tiled<R><<<(unsigned)blocks, kPermThreads, 0, c->stream>>>((const vec2_t<R>*)s->d, (vec2_t<R>*)o->d,
