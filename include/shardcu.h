@@ -216,6 +216,13 @@ int sk_program_nsweeps(const sk_program* p, int* n);
  * n-qubit QFT whose low G qubits are fixed to `value` on this rank (their
  * controlled phases fold into the windows' twiddles).  shift = G; 0 clears. */
 int sk_program_set_phase_index(sk_program* p, int shift, uint64_t value);
+/* Run tiles [tile_begin, tile_end) of one QFT-window sweep (the exchange
+ * overlap of the sharded QFT launches its last body sweep block by block, so
+ * each finished block's transfer starts while the next block computes). */
+int sk_program_run_tiles(sk_state* s, const sk_program* p, int sweep, int64_t tile_begin, int64_t tile_end);
+/* Tile geometry of a sweep: *tile_bits = T (negated when the tiles are not
+ * contiguous index ranges), *tiles = 2^(width - T). */
+int sk_program_sweep_tiles(const sk_program* p, int sweep, int* tile_bits, int64_t* tiles);
 
 /* ---- native hybrid engine (engine.py HybridState, dense shards) ---------
  * The factorised simulator's commit stream runs in C++ next to the kernels:

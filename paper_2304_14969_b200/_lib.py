@@ -102,6 +102,8 @@ _SIGS = {
     "sk_program_run": [p_state, p_prog, C.c_int, C.c_int],
     "sk_program_nsweeps": [p_prog, C.POINTER(C.c_int)],
     "sk_program_set_phase_index": [p_prog, C.c_int, C.c_uint64],
+    "sk_program_run_tiles": [p_state, p_prog, C.c_int, C.c_int64, C.c_int64],
+    "sk_program_sweep_tiles": [p_prog, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int64)],
     "sk_engine_create": [C.c_int, C.POINTER(SkEngineConfig), C.POINTER(p_engine)],
     "sk_engine_destroy": [p_engine],
     "sk_engine_set_rng": [p_engine, UNIFORM_FN, C.c_void_p],

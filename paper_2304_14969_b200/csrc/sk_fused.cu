@@ -712,7 +712,8 @@ struct QSweep {
   int tma;           // last stage stores the tile with one TMA bulk-tensor copy (see k_qft)
   int pshift;        // phase index = (address index << pshift) | pconst (a shard whose low
   uint64_t pconst;   // pshift QFT qubits are rank constants; 0 / 0 otherwise)
-  int pad4, pad5;
+  int tile0;         // first tile of this launch (sk_program_run_tiles; 0 = the whole sweep from tile 0)
+  int pad5;
   Run brun[kQRuns];
   const uint4* thr;  // [nstages][nthreads]
   QStage st[kMaxS];
@@ -861,7 +862,7 @@ __global__ void __launch_bounds__(qft_max_threads<R, NR>(), (qft_min_blocks<R, N
   extern __shared__ __align__(1024) unsigned char smraw[];
   constexpr int NE = 1 << NR;
   const uint32_t tid = threadIdx.x;
-  const uint64_t base = deposit_q(blockIdx.x, sw.brun, sw.nb);
+  const uint64_t base = deposit_q(blockIdx.x + (uint64_t)sw.tile0, sw.brun, sw.nb);
 
   V a[NE];
 #pragma unroll
@@ -1463,7 +1464,7 @@ static int tile_store_map(CUtensorMap* m, void* d, int width, int T, int row_bit
 }
 
 template <typename R, int NR>
-static int launch_one(sk_state* s, const sk_program* p, int i, DevCtx* c) {
+static int launch_one(sk_state* s, const sk_program* p, int i, DevCtx* c, int64_t tb = 0, int64_t te = -1) {
   static bool attr_set[64] = {false};
   if (!attr_set[s->device]) {
 #define SK_ATTR(K) SK_CUDA(cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024))
@@ -1482,15 +1483,21 @@ static int launch_one(sk_state* s, const sk_program* p, int i, DevCtx* c) {
   }
   const DSweep& d = p->sweeps[i];
   const int T = d.ntile;
-  const uint64_t tiles = 1ull << (s->width - T);
+  const uint64_t all_tiles = 1ull << (s->width - T);
+  if (te < 0) te = (int64_t)all_tiles;
+  if (tb < 0 || te > (int64_t)all_tiles || tb >= te)
+    return set_error(SK_EVALUE, "tile range [%lld, %lld) outside sweep %d's %llu tiles", (long long)tb, (long long)te, i,
+                     (unsigned long long)all_tiles);
+  const uint64_t tiles = (uint64_t)(te - tb);
   const unsigned threads = 1u << (T - NR);
   const size_t smem = ((size_t)1 << T) * sizeof(vec2_t<R>);
-  if (tiles > 0x7fffffffull) return set_error(SK_EVALUE, "too many tiles (%d bits outside the tile)", s->width - T);
+  if (all_tiles > 0x7fffffffull) return set_error(SK_EVALUE, "too many tiles (%d bits outside the tile)", s->width - T);
   vec2_t<R>* d_amps = (vec2_t<R>*)s->d;
   // 5-bit c64 and 4-bit c128 sweeps exist only as QFT windows: SK_QFT_KERNEL=0 cannot route them elsewhere
   constexpr bool qft_only = NR > 4 || (sizeof(R) == 8 && NR == 4);
   if (p->qft_ok[i] && threads <= (unsigned)qft_max_threads<R, NR>() && (qft_only || use_qft_kernel())) {
-    const QSweep q = p->pshift ? phase_shifted(p->qsweeps[i], p->pshift, p->pconst) : p->qsweeps[i];
+    QSweep q = p->pshift ? phase_shifted(p->qsweeps[i], p->pshift, p->pconst) : p->qsweeps[i];
+    q.tile0 = (int)tb;
     CUtensorMap tmap{};
     if (q.tma) SK_TRY(tile_store_map(&tmap, s->d, s->width, T, sizeof(vec2_t<R>) == 8 ? 4 : 3));
     switch (q.nstages) {
@@ -1500,6 +1507,8 @@ static int launch_one(sk_state* s, const sk_program* p, int i, DevCtx* c) {
 #undef SK_QS
       default: return set_error(SK_EVALUE, "sweep %d: %d stages", i, q.nstages);
     }
+  } else if (tb != 0 || te != (int64_t)all_tiles) {
+    return set_error(SK_EVALUE, "sweep %d: tile ranges need the QFT-window kernel", i);
   } else if constexpr (NR > 4 || (sizeof(R) == 8 && NR == 4)) {  // 4-bit c128 / 5-bit c64: QFT windows only
     return set_error(SK_EVALUE, "sweep %d: %d register bits need the QFT-window kernel", i, NR);
   } else if (p->pshift) {
@@ -1522,17 +1531,18 @@ static int launch_one(sk_state* s, const sk_program* p, int i, DevCtx* c) {
   return SK_OK;
 }
 
-static int launch_sweeps(sk_state* s, const sk_program* p, int first, int count, DevCtx* c) {
+static int launch_sweeps(sk_state* s, const sk_program* p, int first, int count, DevCtx* c, int64_t tb = 0,
+                         int64_t te = -1) {
   for (int i = first; i < first + count; ++i) {
     const int nr = p->sweeps[i].nr;
     if (s->dtype == SK_C64 && nr == 5) {
-      SK_TRY((launch_one<float, 5>(s, p, i, c)));
+      SK_TRY((launch_one<float, 5>(s, p, i, c, tb, te)));
     } else if (s->dtype == SK_C64) {
-      SK_TRY((launch_one<float, 4>(s, p, i, c)));
+      SK_TRY((launch_one<float, 4>(s, p, i, c, tb, te)));
     } else if (nr == 4) {
-      SK_TRY((launch_one<double, 4>(s, p, i, c)));
+      SK_TRY((launch_one<double, 4>(s, p, i, c, tb, te)));
     } else {
-      SK_TRY((launch_one<double, 3>(s, p, i, c)));
+      SK_TRY((launch_one<double, 3>(s, p, i, c, tb, te)));
     }
   }
   return SK_OK;
@@ -1772,6 +1782,28 @@ int sk_program_run(sk_state* s, const sk_program* p, int first, int count) {
   DevCtx* c;
   SK_TRY(ctx_get(s->device, &c));
   return launch_sweeps(s, p, first, count, c);
+}
+
+int sk_program_run_tiles(sk_state* s, const sk_program* p, int sweep, int64_t tile_begin, int64_t tile_end) {
+  if (!s || !p) return set_error(SK_EVALUE, "null state or program");
+  if (s->width != p->width || s->dtype != p->dtype || s->device != p->device)
+    return set_error(SK_EVALUE, "program planned for width %d dtype %d, state has width %d dtype %d", p->width,
+                     p->dtype, s->width, s->dtype);
+  if (sweep < 0 || sweep >= (int)p->sweeps.size()) return set_error(SK_EVALUE, "sweep %d outside program", sweep);
+  DevCtx* c;
+  SK_TRY(ctx_get(s->device, &c));
+  return launch_sweeps(s, p, sweep, 1, c, tile_begin, tile_end);
+}
+
+int sk_program_sweep_tiles(const sk_program* p, int sweep, int* tile_bits, int64_t* tiles) {
+  if (!p) return set_error(SK_EVALUE, "null program");
+  if (sweep < 0 || sweep >= (int)p->sweeps.size()) return set_error(SK_EVALUE, "sweep %d outside program", sweep);
+  const DSweep& d = p->sweeps[sweep];
+  *tile_bits = d.ntile;
+  *tiles = int64_t(1) << (p->width - d.ntile);
+  // contiguous tiles (the tile is index bits [0, T)): tile t covers [t 2^T, (t+1) 2^T)
+  if (!(d.nb == 0 || (d.nb == 1 && d.brun[0].dst == d.ntile))) *tile_bits = -*tile_bits;
+  return SK_OK;
 }
 
 }  // extern "C"

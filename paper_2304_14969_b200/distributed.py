@@ -218,7 +218,7 @@ class ShardedQFT:
     move device buffers (gloo: the multi-process tests on one GPU)."""
 
     def __init__(self, n_local: int, dtype: str = "c64", group=None, exchange: str = "auto",
-                 chunk_bytes: int = 1 << 30, schedule: str = "one"):
+                 chunk_bytes: int = 1 << 30, schedule: str = "one", overlap: bool = True):
         import torch
         import torch.distributed as dist
 
@@ -237,7 +237,8 @@ class ShardedQFT:
         if exchange not in ("alltoall", "pairwise", "host"):
             raise ValueError(f"exchange must be 'auto', 'alltoall', 'pairwise' or 'host', got {exchange!r}")
         self.exchange = exchange
-        nbuf = 2 if (exchange == "alltoall" and self.G) else 1
+        self.overlap = overlap
+        nbuf = 2 if (exchange in ("alltoall", "host") and self.G) else 1
         self.bufs = [torch.empty(2 << n_local, dtype=real, device=f"cuda:{self.device}") for _ in range(nbuf)]
         self.staging = None
         if exchange == "pairwise" and self.G:
@@ -276,7 +277,8 @@ class ShardedQFT:
             send = self.state.cpu()
             recv = self.torch.empty_like(send)
             self.dist.all_to_all_single(recv, send, group=self.group)
-            self.state.copy_(recv)
+            self.bufs[1 - self.cur].copy_(recv)
+            self.cur = 1 - self.cur
             return
         if self.exchange == "pairwise":
             pairwise_exchange(self.dist, self.bufs[0], self.staging, self.world, self.rank, self.group)
@@ -295,11 +297,84 @@ class ShardedQFT:
             _lib.call("sk_program_run", self._h, self.body._h, i, 1)
             events[i + 1].record(stream)
 
+    def _blocks_of_last_sweep(self):
+        """Tiles per exchange block of the body's last sweep, or None when its
+        tiles are not contiguous index ranges (then no overlap)."""
+        tb, tiles = C.c_int(), C.c_int64()
+        _lib.call("sk_program_sweep_tiles", self.body._h, self.body.n_sweeps - 1, C.byref(tb), C.byref(tiles))
+        if tb.value < 0 or tiles.value % self.world:
+            return None
+        return tiles.value // self.world
+
+    def _post(self, send, dst, recv, src):
+        """Async send/recv pair of one block; returns a completion callable
+        (device tensors over NCCL; host-staged for gloo)."""
+        dist, torch = self.dist, self.torch
+        if self.exchange == "host":
+            s_h, r_h = send.cpu(), torch.empty(recv.shape, dtype=recv.dtype)
+            works = dist.batch_isend_irecv([dist.P2POp(dist.isend, s_h, dst, self.group),
+                                            dist.P2POp(dist.irecv, r_h, src, self.group)])
+
+            def done():
+                for w in works:
+                    w.wait()
+                recv.copy_(r_h)
+            return done
+        works = dist.batch_isend_irecv([dist.P2POp(dist.isend, send, dst, self.group),
+                                        dist.P2POp(dist.irecv, recv, src, self.group)])
+
+        def done():
+            for w in works:
+                w.wait()  # the current stream waits for NCCL's; the host does not block
+        return done
+
+    def _run_overlapped(self, events=None, stream=None) -> bool:
+        """One-exchange schedule with the exchange overlapped: the body's last
+        sweep (the bottom window: contiguous tiles) runs block by block, block
+        b = the amplitudes destined for rank b; as soon as a block is written
+        its transfer is posted (NCCL copies on its own stream) while the next
+        block computes.  Step k sends block rank+k and receives from rank-k,
+        so every step pairs up across ranks.  False when the geometry does not
+        allow it (the caller then runs the plain schedule)."""
+        if not (self.overlap and self.G and self.exchange in ("alltoall", "host")):
+            return False
+        K = self._blocks_of_last_sweep()
+        if K is None:
+            return False
+        W, r, nb = self.world, self.rank, self.body.n_sweeps
+        _lib.call("sk_rebind", self._h, self.state.data_ptr())
+        if events is not None:
+            events[0].record(stream)
+        for i in range(nb - 1):
+            _lib.call("sk_program_run", self._h, self.body._h, i, 1)
+            if events is not None:
+                events[i + 1].record(stream)
+        src_blocks = self.state.view(W, -1)
+        dst_blocks = self.bufs[1 - self.cur].view(W, -1)
+        pending = []
+        for k in range(W):
+            b = (r + k) % W
+            _lib.call("sk_program_run_tiles", self._h, self.body._h, nb - 1, b * K, (b + 1) * K)
+            if k == 0:
+                dst_blocks[r].copy_(src_blocks[r])  # the own block stays
+            else:
+                pending.append(self._post(src_blocks[b], b, dst_blocks[(r - k) % W], (r - k) % W))
+        if events is not None:
+            events[nb].record(stream)
+        for done in pending:
+            done()
+        self.cur = 1 - self.cur
+        _lib.call("sk_rebind", self._h, self.state.data_ptr())
+        _lib.call("sk_program_run", self._h, self.tail._h, 0, -1)
+        return True
+
     def run(self, events=None, stream=None):
         """One sharded QFT on this rank's slab (stream-ordered on the current
         torch stream; libshardcu must be bound to it).  `events` (n_sweeps+1
         CUDA events) bracket the body's fused sweeps for per-launch timing."""
         if self.schedule == "one":
+            if self._run_overlapped(events, stream):
+                return
             self._run_body(events, stream)
             if self.G:
                 self._exchange()
