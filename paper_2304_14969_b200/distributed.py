@@ -234,14 +234,16 @@ class ShardedQFT:
         if exchange == "auto":
             free, _ = torch.cuda.mem_get_info(self.device)
             exchange = "alltoall" if (self.G == 0 or 2 * slab_bytes + (4 << 30) <= free) else "pairwise"
-        if exchange not in ("alltoall", "pairwise", "host"):
-            raise ValueError(f"exchange must be 'auto', 'alltoall', 'pairwise' or 'host', got {exchange!r}")
+        if exchange not in ("alltoall", "pairwise", "host", "host-pairwise"):
+            raise ValueError(f"exchange must be 'auto', 'alltoall', 'pairwise', 'host' or 'host-pairwise', "
+                             f"got {exchange!r}")
         self.exchange = exchange
         self.overlap = overlap
-        nbuf = 2 if (exchange in ("alltoall", "host") and self.G) else 1
+        self._xstream = None
+        nbuf = 2 if (exchange in ("alltoall", "host") and self.G) else 1  # *pairwise: in place, one slab
         self.bufs = [torch.empty(2 << n_local, dtype=real, device=f"cuda:{self.device}") for _ in range(nbuf)]
         self.staging = None
-        if exchange == "pairwise" and self.G:
+        if exchange.endswith("pairwise") and self.G:
             n_stage = min((2 << n_local) // self.world, max(2, chunk_bytes // real.itemsize))
             self.staging = torch.empty(n_stage, dtype=real, device=f"cuda:{self.device}")
         self.cur = 0
@@ -273,6 +275,11 @@ class ShardedQFT:
         return self.bufs[self.cur]
 
     def _exchange(self):
+        if self.exchange == "host-pairwise":
+            blocks = self.state.view(self.world, -1)
+            for k in range(1, self.world):
+                self._pairwise_step(self.rank ^ k, blocks[self.rank ^ k])
+            return
         if self.exchange == "host":
             send = self.state.cpu()
             recv = self.torch.empty_like(send)
@@ -310,7 +317,7 @@ class ShardedQFT:
         """Async send/recv pair of one block; returns a completion callable
         (device tensors over NCCL; host-staged for gloo)."""
         dist, torch = self.dist, self.torch
-        if self.exchange == "host":
+        if self.exchange.startswith("host"):
             s_h, r_h = send.cpu(), torch.empty(recv.shape, dtype=recv.dtype)
             works = dist.batch_isend_irecv([dist.P2POp(dist.isend, s_h, dst, self.group),
                                             dist.P2POp(dist.irecv, r_h, src, self.group)])
@@ -328,20 +335,49 @@ class ShardedQFT:
                 w.wait()  # the current stream waits for NCCL's; the host does not block
         return done
 
+    def _pairwise_step(self, partner: int, blk) -> None:
+        """In-place swap of block `blk` with `partner` (its block for this
+        rank), chunk by chunk through the staging buffer, stream-ordered on the
+        current stream (NCCL: no host wait; gloo: host-staged)."""
+        dist, torch = self.dist, self.torch
+        csz = self.staging.numel() if self.staging is not None else blk.numel()
+        for off in range(0, blk.numel(), csz):
+            n = min(csz, blk.numel() - off)
+            piece = blk[off:off + n]
+            if self.exchange.startswith("host"):
+                s_h, r_h = piece.cpu(), torch.empty(n, dtype=piece.dtype)
+                for w in dist.batch_isend_irecv([dist.P2POp(dist.isend, s_h, partner, self.group),
+                                                 dist.P2POp(dist.irecv, r_h, partner, self.group)]):
+                    w.wait()
+                piece.copy_(r_h)
+                continue
+            into = self.staging[:n]  # (NCCL pairwise)
+            for w in dist.batch_isend_irecv([dist.P2POp(dist.isend, piece, partner, self.group),
+                                             dist.P2POp(dist.irecv, into, partner, self.group)]):
+                w.wait()  # stream wait: the copy below is ordered after the transfer
+            piece.copy_(into)
+
     def _run_overlapped(self, events=None, stream=None) -> bool:
         """One-exchange schedule with the exchange overlapped: the body's last
-        sweep (the bottom window: contiguous tiles) runs block by block, block
-        b = the amplitudes destined for rank b; as soon as a block is written
-        its transfer is posted (NCCL copies on its own stream) while the next
-        block computes.  Step k sends block rank+k and receives from rank-k,
-        so every step pairs up across ranks.  False when the geometry does not
-        allow it (the caller then runs the plain schedule)."""
-        if not (self.overlap and self.G and self.exchange in ("alltoall", "host")):
+        sweep (the bottom window: contiguous tiles) runs block by block on the
+        compute stream, block b = the amplitudes destined for rank b; when a
+        block is written, an exchange stream (waiting on just that block) moves
+        it while the next block computes.  All-to-all (double buffer): step k
+        sends block rank+k and receives from rank-k.  Pairwise in place (one
+        slab, QFT-37 at 128 GiB per GPU): step k swaps block rank^k with the
+        partner's.  False when the geometry does not allow it."""
+        if not (self.overlap and self.G):
             return False
         K = self._blocks_of_last_sweep()
         if K is None:
             return False
+        torch = self.torch
         W, r, nb = self.world, self.rank, self.body.n_sweeps
+        pairwise = self.exchange.endswith("pairwise")
+        comp = torch.cuda.current_stream()  # libshardcu is bound to it
+        if self._xstream is None:
+            self._xstream = torch.cuda.Stream(device=self.device)
+        xs = self._xstream
         _lib.call("sk_rebind", self._h, self.state.data_ptr())
         if events is not None:
             events[0].record(stream)
@@ -350,20 +386,32 @@ class ShardedQFT:
             if events is not None:
                 events[i + 1].record(stream)
         src_blocks = self.state.view(W, -1)
-        dst_blocks = self.bufs[1 - self.cur].view(W, -1)
+        dst_blocks = None if pairwise else self.bufs[1 - self.cur].view(W, -1)
+        order = [r ^ k for k in range(1, W)] + [r] if pairwise else [(r + k) % W for k in range(W)]
         pending = []
-        for k in range(W):
-            b = (r + k) % W
+        for b in order:
             _lib.call("sk_program_run_tiles", self._h, self.body._h, nb - 1, b * K, (b + 1) * K)
-            if k == 0:
-                dst_blocks[r].copy_(src_blocks[r])  # the own block stays
-            else:
-                pending.append(self._post(src_blocks[b], b, dst_blocks[(r - k) % W], (r - k) % W))
+            if b == r:
+                if not pairwise:
+                    dst_blocks[r].copy_(src_blocks[r])  # the own block stays (compute stream)
+                continue
+            ev = torch.cuda.Event()
+            ev.record(comp)
+            xs.wait_event(ev)
+            with torch.cuda.stream(xs):
+                if pairwise:
+                    self._pairwise_step(b, src_blocks[b])
+                else:
+                    src = (2 * r - b) % W  # step k = b - r: receive from rank - k
+                    pending.append(self._post(src_blocks[b], b, dst_blocks[src], src))
         if events is not None:
             events[nb].record(stream)
-        for done in pending:
-            done()
-        self.cur = 1 - self.cur
+        with torch.cuda.stream(xs):
+            for done in pending:
+                done()
+        comp.wait_stream(xs)
+        if not pairwise:
+            self.cur = 1 - self.cur
         _lib.call("sk_rebind", self._h, self.state.data_ptr())
         _lib.call("sk_program_run", self._h, self.tail._h, 0, -1)
         return True

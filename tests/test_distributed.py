@@ -279,7 +279,7 @@ def test_virtual_ranks_one_exchange_large_closed_form():
 # world-size-2 process group: both ranks on cuda:0, gloo with the
 # host-staged exchange (NCCL cannot put two ranks on one device).
 # ---------------------------------------------------------------------------
-def _sharded_run_worker(rank, world, port, n_local, dtype, schedule, q, overlap=True):
+def _sharded_run_worker(rank, world, port, n_local, dtype, schedule, q, overlap=True, exchange="host"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -290,7 +290,7 @@ def _sharded_run_worker(rank, world, port, n_local, dtype, schedule, q, overlap=
         _lib.call("sk_set_stream", 0, stream.cuda_stream)
         n, G = D.layout(n_local, world)
         x = random_state(n, np.random.default_rng(99))
-        sq = D.ShardedQFT(n_local, dtype, exchange="host", schedule=schedule, overlap=overlap)
+        sq = D.ShardedQFT(n_local, dtype, exchange=exchange, schedule=schedule, overlap=overlap, chunk_bytes=4096)
         slab = D.scatter_input(x, world, rank, schedule)
         cplx = torch.complex64 if dtype == "c64" else torch.complex128
         sq.state.copy_(torch.view_as_real(torch.from_numpy(slab).to(cplx)).reshape(-1))
@@ -312,10 +312,12 @@ def _sharded_run_worker(rank, world, port, n_local, dtype, schedule, q, overlap=
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("schedule,overlap", [("one", True), ("one", False), ("two", False)])
+@pytest.mark.parametrize("schedule,overlap,exchange", [("one", True, "host"), ("one", False, "host"),
+                                                      ("one", True, "host-pairwise"), ("one", False, "host-pairwise"),
+                                                      ("two", False, "host")])
 @pytest.mark.parametrize("dtype", ["c128", "c64"])
 @pytest.mark.parametrize("world", [2, 4])
-def test_gloo_sharded_qft_run_on_device(world, dtype, schedule, overlap):
+def test_gloo_sharded_qft_run_on_device(world, dtype, schedule, overlap, exchange):
     """distributed.ShardedQFT.run in a real 2- / 4-process group, vs the DFT of
     the global vector: the one-exchange schedule with the exchange overlapped
     with the last body sweep (block-by-block launches + per-block async
@@ -324,7 +326,8 @@ def test_gloo_sharded_qft_run_on_device(world, dtype, schedule, overlap):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_sharded_run_worker, args=(r, world, port, n_local, dtype, schedule, q, overlap))
+    procs = [ctx.Process(target=_sharded_run_worker,
+                         args=(r, world, port, n_local, dtype, schedule, q, overlap, exchange))
              for r in range(world)]
     for p in procs:
         p.start()
