@@ -258,16 +258,33 @@ typedef struct {
 #define SK_ENGINE_STAT_PEAK 8        /* peak_amplitudes */
 #define SK_ENGINE_STAT_NEPS 9        /* len(eps_record) */
 #define SK_ENGINE_STAT_NEEDED 10     /* `needed` of the last SK_EBUDGET */
-#define SK_ENGINE_NSTATS 11
+#define SK_ENGINE_STAT_DIST_SHARDS 11 /* shards split over the ranks (sk_engine_set_distributed) */
+#define SK_ENGINE_STAT_EXCHANGES 12  /* rank-bit <-> slab-bit swaps of distributed shards */
+#define SK_ENGINE_NSTATS 13
 
 typedef double (*sk_uniform_fn)(void* ctx); /* rng.random() of the caller's PCG64 stream */
 typedef int (*sk_bit_fn)(void* ctx);        /* rng.integers(0, 2) of the same stream (tableau measurements) */
+/* collectives of the distributed largest shard, provided by the host's
+ * process group (torch.distributed: NCCL on the box, gloo in the tests);
+ * each returns 0 on success and completes before returning */
+typedef int (*sk_allreduce_fn)(void* ctx, double* x, int n); /* in-place sum over ranks of n host doubles */
+typedef int (*sk_sendrecv_fn)(void* ctx, int partner, uint64_t send_dev, uint64_t recv_dev, int64_t nbytes);
+typedef int (*sk_allgather_fn)(void* ctx, uint64_t send_dev, uint64_t recv_dev, int64_t nbytes_per_rank);
 
 /* HybridState(n, cfg) (engine.py:164-182): n width-1 shards |0>. */
 int sk_engine_create(int n, const sk_engine_config* cfg, sk_engine** out);
 int sk_engine_destroy(sk_engine* e);
 int sk_engine_set_rng(sk_engine* e, sk_uniform_fn fn, void* ctx);
 int sk_engine_set_rng_bits(sk_engine* e, sk_bit_fn fn, void* ctx);
+/* SPMD distribution: every rank runs the same engine on the
+ * same circuit; a dense shard wider than local_max_width is split over the
+ * `world` ranks by its top log2(world) positions (merges with replicated
+ * shards grow every slab locally; gates, Bloch sums and SDRP rounding act on
+ * local positions, rank-bit qubits are swapped into the slab by pairwise
+ * exchanges; reductions are summed over ranks, so every rank takes the same
+ * decisions) and gathered back once it narrows to local_max_width. */
+int sk_engine_set_distributed(sk_engine* e, int world, int rank, int local_max_width, sk_allreduce_fn allreduce,
+                              sk_sendrecv_fn sendrecv, sk_allgather_fn allgather, void* ctx);
 /* apply_gate for gates [0, ngates) (engine.py:514-573): kind[g], targets[2g..2g+1],
  * controls ctrls[ctrl_off[g] .. ctrl_off[g+1]) with polarities pols[...], matrix mats[8g..8g+7].
  * *done = gates fully applied (the failing gate is not counted). */

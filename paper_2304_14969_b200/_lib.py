@@ -46,9 +46,12 @@ class SkEngineConfig(C.Structure):
 
 SK_GATE_1Q, SK_GATE_SWAP, SK_GATE_MEASURE = 0, 1, 2
 ENGINE_STATS = ("label_swaps", "kernels", "eliminated_controls", "merges", "splits", "allocs", "amplitude_writes",
-                "dense_total", "peak_amplitudes", "n_eps", "needed")
+                "dense_total", "peak_amplitudes", "n_eps", "needed", "dist_shards", "exchanges")
 UNIFORM_FN = C.CFUNCTYPE(C.c_double, C.c_void_p)
 BIT_FN = C.CFUNCTYPE(C.c_int, C.c_void_p)
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int)
+SENDRECV_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_uint64, C.c_uint64, C.c_int64)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint64, C.c_uint64, C.c_int64)
 p_engine = C.c_void_p
 i32p = C.POINTER(C.c_int32)
 
@@ -108,6 +111,8 @@ _SIGS = {
     "sk_engine_destroy": [p_engine],
     "sk_engine_set_rng": [p_engine, UNIFORM_FN, C.c_void_p],
     "sk_engine_set_rng_bits": [p_engine, BIT_FN, C.c_void_p],
+    "sk_engine_set_distributed": [p_engine, C.c_int, C.c_int, C.c_int, ALLREDUCE_FN, SENDRECV_FN, ALLGATHER_FN,
+                                  C.c_void_p],
     "sk_engine_apply": [p_engine, C.c_int, i32p, i32p, i32p, i32p, i32p, dptr, C.POINTER(C.c_int)],
     "sk_engine_measure": [p_engine, C.c_int, C.POINTER(C.c_int)],
     "sk_engine_flush_all": [p_engine],

@@ -179,11 +179,13 @@ struct SumsTicket {
 };
 
 struct Shard {
-  sk_state* st = nullptr;                 // dense shards
+  sk_state* st = nullptr;                 // dense shards (a distributed shard: this rank's slab)
   std::unique_ptr<sktab::Tableau> tab;    // stabilizer shards (engine.py Shard kind "stab")
   std::vector<Qubit*> qubits;  // position -> qubit
   SumsTicket sums;             // width-1 shards only
+  int G = 0;                   // distributed over 2^G ranks: positions [w-G, w) are the rank bits
   int width() const { return (int)qubits.size(); }
+  int wl() const { return width() - G; }  // local positions [0, wl) = bits of this rank's slab
   bool stab() const { return (bool)tab; }
 };
 
@@ -303,6 +305,19 @@ __global__ void __launch_bounds__(kEThreads) k_e_kron_narrow(const vec2_t<R>* __
   }
 }
 
+// this rank's slab of a product that becomes distributed: out[i] = prod[base + i]
+template <typename R>
+__global__ void __launch_bounds__(kEThreads) k_e_kron_slice(const vec2_t<R>* __restrict__ lo,
+                                                           const vec2_t<R>* __restrict__ hi, vec2_t<R>* __restrict__ out,
+                                                           int64_t n, int wa, uint64_t base) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const uint64_t mask = (1ull << wa) - 1;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint64_t j = base + (uint64_t)i;
+    out[i] = cmul<R>(hi[j >> wa], lo[j & mask]);
+  }
+}
+
 // SDRP rounding split (engine.py:464-488) in one launch: the remainder
 // rest[k] = (u00 a0[k] + u01 a1[k]) / sqrt(P0) and the new width-1 shard phi
 // with its published Bloch sums
@@ -345,6 +360,15 @@ struct sk_engine {
   void* uctx = nullptr;
   sk_bit_fn bfn = nullptr;  // rng.integers(0, 2): tableau measurements (tableau.py:214)
   void* bctx = nullptr;
+  // distributed largest shard: SPMD over `world` ranks, every
+  // rank runs this engine on the same circuit; a dense shard wider than
+  // local_max is split over the ranks by its top log2(world) positions and its
+  // reductions are summed over ranks, so all ranks take the same decisions
+  int world = 1, rank = 0, Gw = 0, local_max = 64;
+  sk_allreduce_fn f_allreduce = nullptr;
+  sk_sendrecv_fn f_sendrecv = nullptr;
+  sk_allgather_fn f_allgather = nullptr;
+  void* dctx = nullptr;
   double* h_ring = nullptr;  // mapped pinned ring of sums slots
   double* d_ring = nullptr;
   int ring_next = 0;
@@ -559,6 +583,127 @@ struct sk_engine {
     return SK_OK;
   }
 
+  // ---- distributed shard (row f2) -------------------------------------------------
+  int sync_stream() {
+    SK_CUDA(cudaStreamSynchronize(ctx->stream));
+    return SK_OK;
+  }
+
+  int allreduce(double* x, int n) {  // sum over ranks (every rank gets the same doubles)
+    if (world == 1) return SK_OK;
+    if (f_allreduce(dctx, x, n) != 0) return set_error(SK_ECUDA, "distributed all-reduce failed");
+    return SK_OK;
+  }
+
+  // bring the qubit at global position pos into the slab: swap its rank bit
+  // with the top local bit (first moving a non-busy local qubit there);
+  // partners exchange the half slab whose top bit disagrees with their rank bit
+  int localize(Shard* s, int pos, const std::vector<int>& busy) {
+    const int wl = s->wl();
+    if (pos < wl) return SK_OK;
+    int v = -1;
+    for (int p = wl - 1; p >= 0 && v < 0; --p)
+      if (std::find(busy.begin(), busy.end(), p) == busy.end()) v = p;
+    if (v < 0) return set_error(SK_EVALUE, "distributed shard: no free local qubit to swap with");
+    if (v != wl - 1) {  // a local bit swap puts the victim on top (one slab pass)
+      SK_TRY(sk_swap_qubits(s->st, v, wl - 1));
+      std::swap(s->qubits[v], s->qubits[wl - 1]);
+      s->qubits[v]->pos = v;
+      s->qubits[wl - 1]->pos = wl - 1;
+    }
+    const int g = pos - wl;
+    const int rb = (rank >> g) & 1, partner = rank ^ (1 << g);
+    const size_t half = ((size_t)1 << (wl - 1)) * s->st->elem;
+    unsigned char* mine = (unsigned char*)s->st->d + (size_t)(1 - rb) * half;
+    void* tmp = nullptr;
+    SK_CUDA(cudaMallocAsync(&tmp, half, ctx->stream));
+    SK_TRY(sync_stream());
+    const int rc = f_sendrecv(dctx, partner, (uint64_t)mine, (uint64_t)tmp, (int64_t)half);
+    if (rc != 0) {
+      cudaFreeAsync(tmp, ctx->stream);
+      return set_error(SK_ECUDA, "distributed exchange with rank %d failed", partner);
+    }
+    SK_CUDA(cudaMemcpyAsync(mine, tmp, half, cudaMemcpyDeviceToDevice, ctx->stream));
+    SK_CUDA(cudaFreeAsync(tmp, ctx->stream));
+    std::swap(s->qubits[wl - 1], s->qubits[pos]);
+    s->qubits[wl - 1]->pos = wl - 1;
+    s->qubits[pos]->pos = pos;
+    stats[SK_ENGINE_STAT_EXCHANGES]++;
+    return SK_OK;
+  }
+
+  // a distributed shard narrow enough for one device again (or any, for a
+  // read-out): all-gather the slabs
+  int undistribute(Shard* s, bool force = false) {
+    if (!s->G || (s->width() > local_max && !force)) return SK_OK;
+    sk_state* full;
+    SK_TRY(alloc_state(s->width(), &full));
+    const size_t bytes = (size_t)s->st->n * s->st->elem;
+    SK_TRY(sync_stream());
+    if (f_allgather(dctx, (uint64_t)s->st->d, (uint64_t)full->d, (int64_t)bytes) != 0)
+      return set_error(SK_ECUDA, "distributed all-gather failed");
+    free_state(s->st);
+    s->st = full;
+    s->G = 0;
+    return SK_OK;
+  }
+
+  int dist_product(Shard* a, Shard* b, Shard** out) {  // a (wider) x b wider than local_max: split it
+    const int wa = a->width(), wb = b->width(), w = wa + wb, wl = w - Gw;
+    if (wl < 2) return set_error(SK_EVALUE, "distributed shard of %d qubits over %d ranks is too narrow", w, world);
+    SK_TRY(charge(int64_t(1) << w));
+    sk_state* st;
+    SK_TRY(alloc_state(wl, &st));
+    const int64_t n = int64_t(1) << wl;
+    const int g = grid_for(n, kEThreads, 2, ctx->num_sms);
+    const uint64_t base = (uint64_t)rank << wl;
+    if (cfg.dtype == SK_C64)
+      k_e_kron_slice<float><<<g, kEThreads, 0, ctx->stream>>>((const float2*)a->st->d, (const float2*)b->st->d,
+                                                               (float2*)st->d, n, wa, base);
+    else
+      k_e_kron_slice<double><<<g, kEThreads, 0, ctx->stream>>>((const double2*)a->st->d, (const double2*)b->st->d,
+                                                                (double2*)st->d, n, wa, base);
+    SK_CHECK_LAUNCH();
+    SK_TRY(merged_shard(a, b, st, out));
+    (*out)->G = Gw;  // positions [wl, w): the top Gw positions are the rank bits
+    stats[SK_ENGINE_STAT_DIST_SHARDS]++;
+    return SK_OK;
+  }
+
+  int dist_kron(Shard* d, Shard* r, Shard** out) {  // distributed d x replicated r: each slab grows locally
+    if (r->G) return set_error(SK_EVALUE, "merging two distributed shards is not supported");
+    const int wl = d->wl(), wr = r->width(), w = d->width() + wr;
+    SK_TRY(charge(int64_t(1) << w));
+    sk_state* st;
+    SK_TRY(alloc_state(wl + wr, &st));
+    const int64_t n = int64_t(1) << (wl + wr);
+    const int g = grid_for(n, kEThreads, 2, ctx->num_sms);
+    if (cfg.dtype == SK_C64)
+      k_e_kron<float><<<g, kEThreads, 0, ctx->stream>>>((const float2*)d->st->d, (const float2*)r->st->d,
+                                                         (float2*)st->d, n, wl);
+    else
+      k_e_kron<double><<<g, kEThreads, 0, ctx->stream>>>((const double2*)d->st->d, (const double2*)r->st->d,
+                                                          (double2*)st->d, n, wl);
+    SK_CHECK_LAUNCH();
+    stats[SK_ENGINE_STAT_MERGES]++;
+    stats[SK_ENGINE_STAT_WRITES] += int64_t(1) << w;
+    SK_TRY(release((int64_t(1) << d->width()) + (int64_t(1) << wr)));
+    Shard* m = new_shard(st);
+    // positions: d's local, r's (new local bits above them), d's rank bits on top
+    m->qubits.assign(d->qubits.begin(), d->qubits.begin() + wl);
+    m->qubits.insert(m->qubits.end(), r->qubits.begin(), r->qubits.end());
+    m->qubits.insert(m->qubits.end(), d->qubits.begin() + wl, d->qubits.end());
+    m->G = d->G;
+    for (int i = 0; i < m->width(); ++i) {
+      m->qubits[i]->shard = m;
+      m->qubits[i]->pos = i;
+    }
+    drop_shard(d);
+    drop_shard(r);
+    *out = m;
+    return SK_OK;
+  }
+
   int merge_pair(Shard* a, Shard* b, Shard** out, bool stab_ok = false) {  // engine.py:224-243
     if (a->width() < b->width()) std::swap(a, b);  // the wider keeps its positions
     if (stab_ok && a->stab() && b->stab()) {
@@ -582,6 +727,8 @@ struct sk_engine {
     SK_TRY(to_dense(a));
     SK_TRY(to_dense(b));
     const int wa = a->width(), wb = b->width();
+    if (a->G || b->G) return a->G ? dist_kron(a, b, out) : dist_kron(b, a, out);
+    if (world > 1 && wa + wb > local_max) return dist_product(a, b, out);
     SK_TRY(charge(int64_t(1) << (wa + wb)));
     sk_state* st;
     SK_TRY(alloc_state(wa + wb, &st));
@@ -641,7 +788,7 @@ struct sk_engine {
   }
 
   // replace shard by (rest, new width-1 shard {single}) (engine.py:257-270)
-  void split(Shard* shard, int pos, sk_state* single, const SumsTicket& single_sums, sk_state* rest) {
+  int split(Shard* shard, int pos, sk_state* single, const SumsTicket& single_sums, sk_state* rest) {
     Qubit* q = shard->qubits[pos];
     const int64_t old = int64_t(1) << shard->width();
     stats[SK_ENGINE_STAT_SPLITS]++;
@@ -655,7 +802,8 @@ struct sk_engine {
     free_state(shard->st);
     shard->st = rest;
     shard->sums.kind = kSumsNone;
-    dense_total += (2 + (int64_t(1) << rest->width)) - old;
+    dense_total += (2 + (int64_t(1) << shard->width())) - old;  // global widths (a distributed rest is a slab)
+    return undistribute(shard);
   }
 
   // Bloch sums of q in its shard: width-1 shards carry them (host values or
@@ -677,6 +825,11 @@ struct sk_engine {
     if (s->width() == 1 && s->sums.kind == kSumsHost) {
       std::copy(s->sums.v, s->sums.v + 4, out);
       return SK_OK;
+    }
+    if (s->G) {  // a distributed shard: local reduction on every rank, summed over ranks
+      SK_TRY(localize(s, q->pos, {}));
+      SK_TRY(sk_bloch_sums(s->st, q->pos, out));
+      return allreduce(out, 4);
     }
     SK_TRY(sk_bloch_sums(s->st, q->pos, out));
     if (s->width() == 1) {
@@ -745,6 +898,7 @@ struct sk_engine {
     if (!unitary(m)) return set_error(SK_EVALUE, "matrix is not unitary within 1e-10");
     double m8[8];
     m_to8(m, m8);
+    if (s->G) SK_TRY(localize(s, q->pos, {}));
     SK_TRY(sk_apply_1q(s->st, q->pos, m8));
     stats[SK_ENGINE_STAT_KERNELS]++;
     stats[SK_ENGINE_STAT_WRITES] += int64_t(1) << s->width();
@@ -834,8 +988,17 @@ struct sk_engine {
       if (!unitary(m)) return set_error(SK_EVALUE, "matrix is not unitary within 1e-10");
       double m8[8];
       m_to8(m, m8);
+      if (s->G) {  // every operand into this rank's slab (rank-bit operands are swapped in)
+        for (Qubit* q : qs) {
+          std::vector<int> busy;
+          for (Qubit* o : qs)
+            if (o != q && o->pos < s->wl()) busy.push_back(o->pos);
+          SK_TRY(localize(s, q->pos, busy));
+        }
+      }
       if (controls.size() == 1) {
         SK_TRY(sk_apply_controlled_bloch(s->st, controls[0]->pos, pol[0], target->pos, m8, out8));
+        if (s->G) SK_TRY(allreduce(out8, 8));
         stats[SK_ENGINE_STAT_WRITES] += int64_t(1) << (s->width() - 1);
       } else {
         uint64_t mask = 0, val = 0;
@@ -920,6 +1083,7 @@ struct sk_engine {
     const bool merge = sa != sb;
     const int w = merge ? sa->width() + sb->width() : sa->width();
     if (w > kFusedMaxW) return SK_OK;
+    if (world > 1 && (sa->G || sb->G || w > local_max)) return SK_OK;  // distributed: the general path
     CouplerArgs A{};
     for (Qubit* q : {c, t}) {  // commit_1q of each operand (engine.py:305-322)
       if (!q->has_u) continue;
@@ -1045,7 +1209,7 @@ struct sk_engine {
     sk_state* single;
     SumsTicket ss;
     SK_TRY(make_single(phi, &single, &ss));
-    split(shard, pos, single, ss, rest);
+    SK_TRY(split(shard, pos, single, ss, rest));
     *done = true;
     return SK_OK;
   }
@@ -1067,7 +1231,7 @@ struct sk_engine {
     const double p0 = std::norm(u.a[0]) * sums[2] + std::norm(u.a[1]) * sums[3] +
                       2.0 * (std::conj(u.a[0]) * u.a[1] * cross).real();
     if (p0 < 1e-12) return SK_OK;  // numerically degenerate: leave the state alone (engine.py:477-480)
-    const int w = shard->width();
+    const int w = shard->wl();  // the slab (a distributed shard rounds a local qubit on every rank)
     sk_state *rest, *single;
     SK_TRY(alloc_state(w - 1, &rest));
     SK_TRY(alloc_state(1, &single));
@@ -1090,8 +1254,8 @@ struct sk_engine {
           mk<double>(u.a[1].real(), u.a[1].imag()), scale, (double2*)single->d, phi[0].real(), phi[0].imag(),
           phi[1].real(), phi[1].imag(), dslot, dflag, ss.seq);
     SK_CHECK_LAUNCH();
-    stats[SK_ENGINE_STAT_WRITES] += int64_t(1) << w;
-    split(shard, pos, single, ss, rest);
+    stats[SK_ENGINE_STAT_WRITES] += int64_t(1) << shard->width();
+    SK_TRY(split(shard, pos, single, ss, rest));
     if (eps > cfg.separability_tol) eps_push(eps);
     *rounded = true;
     return SK_OK;
@@ -1184,7 +1348,7 @@ struct sk_engine {
       sk_state* single;
       SumsTicket ss;
       SK_TRY(make_single(basis, &single, &ss));
-      split(s, h->pos, single, ss, rest);
+      SK_TRY(split(s, h->pos, single, ss, rest));
     } else {
       double prob;
       SK_TRY(sk_project(s->st, h->pos, out, &prob));
@@ -1258,6 +1422,19 @@ struct sk_engine {
     for (Qubit* h : handles) {
       Shard* s = h->shard;
       if (!seen.insert(s).second || s->stab()) continue;
+      if (s->G) {  // the layer's qubits into this rank's slab first
+        std::vector<Qubit*> paulis;
+        for (Qubit* qb : s->qubits) {
+          cd ph;
+          if (qb->has_u && as_pauli(qb->u, &ph) >= 0) paulis.push_back(qb);
+        }
+        for (Qubit* qb : paulis) {
+          std::vector<int> busy;
+          for (Qubit* o : paulis)
+            if (o != qb && o->pos < s->wl()) busy.push_back(o->pos);
+          SK_TRY(localize(s, qb->pos, busy));
+        }
+      }
       uint64_t flip = 0, sign = 0;
       int y = 0, count = 0, first_pos = -1, first_p = -1;
       cd scale = 1.0;
@@ -1422,6 +1599,28 @@ int sk_engine_eps(const sk_engine* e, double* out, int64_t cap) {
   return SK_OK;
 }
 
+int sk_engine_set_distributed(sk_engine* e, int world, int rank, int local_max_width, sk_allreduce_fn allreduce,
+                              sk_sendrecv_fn sendrecv, sk_allgather_fn allgather, void* ctx) {
+  SK_TRY(check_engine(e));
+  int G = 0;
+  while ((1 << G) < world) ++G;
+  if (world < 1 || (1 << G) != world) return set_error(SK_EVALUE, "world size must be a power of two, got %d", world);
+  if (rank < 0 || rank >= world) return set_error(SK_EVALUE, "rank %d outside world %d", rank, world);
+  if (world > 1 && (!allreduce || !sendrecv || !allgather)) return set_error(SK_EVALUE, "missing collective callbacks");
+  if (local_max_width < G + 2) return set_error(SK_EVALUE, "local_max_width must be >= log2(world) + 2");
+  for (Shard* sh : e->shards)
+    if (sh->G) return set_error(SK_EVALUE, "set the distribution before any shard is distributed");
+  e->world = world;
+  e->rank = rank;
+  e->Gw = G;
+  e->local_max = local_max_width;
+  e->f_allreduce = allreduce;
+  e->f_sendrecv = sendrecv;
+  e->f_allgather = allgather;
+  e->dctx = ctx;
+  return SK_OK;
+}
+
 int sk_engine_set_rng_bits(sk_engine* e, sk_bit_fn fn, void* ctx) {
   SK_TRY(check_engine(e));
   e->bfn = fn;
@@ -1431,6 +1630,7 @@ int sk_engine_set_rng_bits(sk_engine* e, sk_bit_fn fn, void* ctx) {
 
 int sk_engine_shards(sk_engine* e, int cap, sk_state** states, int* widths, int* labels, int* owned, int* nshards) {
   SK_TRY(check_engine(e));
+  for (Shard* sh : std::vector<Shard*>(e->shards.begin(), e->shards.end())) SK_TRY(e->undistribute(sh, true));
   // shards in order of their lowest label (engine.py _shards_in_label_order);
   // labels[] lists each shard's qubits by position, shard after shard; a
   // tableau shard is handed out as a fresh dense ket (owned[i] = 1, the
@@ -1511,6 +1711,7 @@ int sk_engine_load_state(sk_engine* e, const sk_state* s) {  // engine.py:768-78
 int sk_engine_measure_all(sk_engine* e, uint8_t* bits) {  // engine.py:596-626
   SK_TRY(check_engine(e));
   SK_TRY(e->flush_all());
+  for (Shard* sh : std::vector<Shard*>(e->shards.begin(), e->shards.end())) SK_TRY(e->undistribute(sh, true));
   std::vector<Shard*> order;
   for (int l = 0; l < e->n; ++l) {
     Shard* s = e->handles[l]->shard;
@@ -1552,6 +1753,7 @@ int sk_engine_sample(sk_engine* e, int64_t shots, uint8_t* bits) {  // engine.py
   SK_TRY(check_engine(e));
   if (shots < 0) return set_error(SK_EVALUE, "negative shot count");
   SK_TRY(e->flush_all());
+  for (Shard* sh : std::vector<Shard*>(e->shards.begin(), e->shards.end())) SK_TRY(e->undistribute(sh, true));
   std::vector<Shard*> order;
   for (int l = 0; l < e->n; ++l) {
     Shard* s = e->handles[l]->shard;

@@ -4,6 +4,7 @@ are checked against a real world-size-2/4 gloo all_to_all_single."""
 from __future__ import annotations
 
 import os
+from pathlib import Path
 import socket
 
 import numpy as np
@@ -408,3 +409,90 @@ def test_gloo_sharded_state_circuits(world, n, dtype, kind):
     assert abs(norm2 - 1.0) < (1e-12 if dtype == "c128" else 1e-5)
     assert perr < tol
     assert exchanges > 0  # global qubits really were brought home
+
+
+# ---------------------------------------------------------------------------
+# Distributed largest shard: the native engine SPMD over a
+# process group; shards wider than local_max_width are split over the ranks.
+# The decisions must be the reference engine's (tests/golden/engine.npz and
+# the 54q SDRP goldens) on every rank.
+# ---------------------------------------------------------------------------
+def _dist_engine_worker(rank, world, port, local_max, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2304_14969_b200 import _lib
+        from paper_2304_14969_b200.circuit import build_random_circuit
+        from paper_2304_14969_b200.engine import EngineConfig, HybridState, OptFlags
+        from paper_2304_14969_b200.errors import MemoryBudgetError
+        torch.cuda.set_device(0)
+        _lib.call("sk_set_stream", 0, torch.cuda.current_stream().cuda_stream)
+        eg = np.load(Path(__file__).resolve().parent / "golden" / "engine.npz")
+        results = []
+        keys = sorted({k.rsplit("/", 1)[0] for k in eg.files if k.startswith("eng/")})
+        for key in keys:
+            w, dep, seed, budget = (int(v) for v in eg[f"{key}/spec"])
+            if w < local_max + 2 or not bool(eg[f"{key}/ok"]):
+                continue
+            fl = OptFlags(*[bool(b) for b in eg[f"{key}/flags"]])
+            cfg = EngineConfig(sdrp=float(eg[f"{key}/p"]), mem_budget=budget, rng_seed=seed, optimizations=fl)
+            sim = HybridState(w, cfg, local_max_width=local_max)
+            sim.apply_circuit(build_random_circuit(w, dep, seed))
+            sim.flush_all()
+            ket = sim.full_ket().amps
+            results.append((key, sim.eps_record, sim.peak_amplitudes, [sim.stats[s] for s in
+                            ("label_swaps", "kernels", "eliminated_controls", "merges", "splits")],
+                            float(np.max(np.abs(ket - eg[f"{key}/ket"]))), sim.distribution))
+        # a 54-qubit SDRP run at the golden's p_min (circuit 2, budget 2^18)
+        g54 = eg["minsdrp/54_7_2/spec"]
+        w, dep, seed, budget = (int(v) for v in g54)
+        p_min = float(eg["minsdrp/54_7_2/res"][1])
+        sim = HybridState(w, EngineConfig(sdrp=p_min, mem_budget=budget, rng_seed=seed), local_max_width=local_max + 4)
+        sim.apply_circuit(build_random_circuit(w, dep, seed))
+        sim.flush_all()
+        results.append(("54q", sim.eps_record, sim.peak_amplitudes, sim.stats["merges"], 0.0, sim.distribution))
+        q.put((rank, results))
+    except Exception as exc:
+        import traceback
+        q.put((rank, repr(exc) + traceback.format_exc()))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,local_max", [(2, 6), (4, 7)])
+def test_gloo_distributed_largest_shard_engine(golden, world, local_max):
+    eg = golden("engine")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dist_engine_worker, args=(r, world, port, local_max, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    try:
+        out = dict(q.get(timeout=600) for _ in range(world))
+    finally:
+        for p in procs:
+            p.join(timeout=60)
+            if p.is_alive():
+                p.kill()
+    for r in range(world):
+        assert not isinstance(out[r], str), out[r]
+    ref = out[0]
+    assert len(ref) >= 10
+    assert sum(d["dist_shards"] for *_, d in ref) >= 5 and sum(d["exchanges"] for *_, d in ref) >= 5, \
+        [d for *_, d in ref]  # shards really were split over the ranks and rank bits swapped in
+    assert ref[-1][-1]["dist_shards"] > 0  # the 54-qubit run too
+    for key, eps, peak, stats, kerr, _ in ref:
+        if key == "54q":
+            np.testing.assert_allclose(eps, eg["minsdrp/54_7_2/eps"], atol=1e-9)
+            assert peak == int(eg["minsdrp/54_7_2/res"][3])
+            continue
+        np.testing.assert_allclose(eps, eg[f"{key}/eps"], atol=1e-9, err_msg=key)
+        assert peak == int(eg[f"{key}/peak"]), key
+        assert stats == [int(v) for v in eg[f"{key}/stats"]], key
+        assert kerr < 1e-10, (key, kerr)
+    for r in range(1, world):  # every rank took the same decisions
+        for a, b in zip(ref, out[r]):
+            assert a[0] == b[0] and np.array_equal(a[1], b[1]) and a[2] == b[2], (r, a[0])
