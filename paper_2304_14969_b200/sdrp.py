@@ -16,9 +16,12 @@ from .ket import DenseKet
 DEFAULT_P_STEP = 0.025
 
 
-def run_hybrid(c: Circuit, cfg: EngineConfig, initial: DenseKet | None = None) -> HybridState:
-    """validate.py:114-121."""
-    sim = HybridState(c.width, cfg)
+def run_hybrid(c: Circuit, cfg: EngineConfig, initial: DenseKet | None = None, group=None,
+               local_max_width: int | None = None) -> HybridState:
+    """validate.py:114-121.  With `local_max_width` (inside an initialised
+    torch.distributed group, every rank calling it) the largest shard is
+    split over the ranks once wider than that (sk_engine_set_distributed)."""
+    sim = HybridState(c.width, cfg, group=group, local_max_width=local_max_width)
     if initial is not None:
         sim.load_state(initial)
     sim.apply_circuit(c)
@@ -51,7 +54,8 @@ class SdrpRun:
 
 
 def min_sdrp_search(width: int, depth: int, seed: int, mem_budget: int, p_step: float = DEFAULT_P_STEP,
-                    dtype: str = "c128", trace: list | None = None) -> MinSdrpResult:
+                    dtype: str = "c128", trace: list | None = None, group=None,
+                    local_max_width: int | None = None) -> MinSdrpResult:
     """Lower p from 1 in p_step decrements until the budget fails; report the
     last completing run (validate.py:280-300)."""
     if p_step <= 0:
@@ -64,7 +68,7 @@ def min_sdrp_search(width: int, depth: int, seed: int, mem_budget: int, p_step: 
         cfg = EngineConfig(sdrp=p, mem_budget=mem_budget, rng_seed=seed, dtype=dtype)
         t0 = time.perf_counter()
         try:
-            sim = run_hybrid(c, cfg)
+            sim = run_hybrid(c, cfg, group=group, local_max_width=local_max_width)
             sim.flush_all()
         except MemoryBudgetError as exc:
             if trace is not None:
