@@ -25,7 +25,7 @@ esz = 8 if dtype == "c64" else 16
 tiles = [int(t) for t in os.environ["TILES"].split(",")] if "TILES" in os.environ else (
     [11, 12, 13] if dtype == "c64" else [10, 11, 12])
 for T in tiles:
-    for low in (3, 4, 5):
+    for low in ([int(x) for x in os.environ["LOWS"].split(",")] if "LOWS" in os.environ else (3, 4, 5)):
         try:
             kw = {"qft_nreg": int(os.environ["QFT_NREG"])} if "QFT_NREG" in os.environ else {}
             prog = compile_circuit(c, dtype=dtype, tile_bits=T, low_bits=low, **kw)
