@@ -50,8 +50,13 @@ def _deps(src: Path, seen: set | None = None) -> set:
     return seen
 
 
+# scripts/dev_build.py links a reduced development library (c64 generic
+# sweeps only); its marker forces the next regular build
+DEV_MARKER = ROOT / "build" / "DEV_LIB"
+
+
 def is_stale() -> bool:
-    if not LIB.exists():
+    if not LIB.exists() or DEV_MARKER.exists():
         return True
     t = LIB.stat().st_mtime
     return any(p.stat().st_mtime > t for p in sources() + headers())
@@ -89,6 +94,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)
     os.replace(tmp, LIB)
+    DEV_MARKER.unlink(missing_ok=True)
     return LIB
 
 

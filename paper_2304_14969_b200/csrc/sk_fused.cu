@@ -30,7 +30,9 @@
 #include <cuda.h>  // CUtensorMap (types only; the encoder comes via cudaGetDriverEntryPoint)
 #include <cudaTypedefs.h>
 
+#include <cmath>
 #include <cstdlib>
+#include <type_traits>
 #include <vector>
 
 #include "sk_internal.cuh"
@@ -90,7 +92,13 @@ enum KOpc : uint32_t {
   OPC_MATQ = 16,   // + 2 (4P + Q) + V: dense 2x2 on slot P where register slot Q == V
   OPC_SWAPQ = 48,  // + 2 (4P + Q) + V: X on slot P where register slot Q == V
   OPC_PHASE = 80,  // K_PHASE with a specialised element pattern
-  OPC_END = 81
+  OPC_SIGN = 81,   // K_PHASE by -1 (CZ-type couplers): sign-bit flips on the pattern's elements
+  OPC_YSWAPT = 82,  // + P: Y on slot P (swap with +-i: register moves and sign flips), thread predicate
+  OPC_YSWAPQ = 86,  // + 2 (4P + Q) + V: Y on slot P where register slot Q == V
+  OPC_MATR = 118,   // + P: real 2x2 on slot P, unpredicated (the R_y factor of a split 1q gate)
+  OPC_DIAG1 = 122,  // + 2P + V: phase on the elements whose slot P == V, unpredicated
+  OPC_MATRP = 130,  // + P: 2x2 with a real first column = real rotation after a phase on a1
+  OPC_END = 134
 };
 
 template <typename R>
@@ -495,18 +503,10 @@ __device__ __forceinline__ void apply_kop(const KOp<R>* __restrict__ op, vec2_t<
   }
 }
 
-// unpredicated dense 2x2 on slot P: coefficients m and rotated mr as four
-// 16-byte loads, then 8 (fp32) paired ops per element pair
+// unpredicated dense 2x2 on slot P from c[0..7] = m00 r00 m01 r01 m10 r10 m11 r11
+// (r = m rotated by i): 8 (fp32) paired ops per element pair
 template <typename R, int NR, int P>
-__device__ __forceinline__ void mat_full(vec2_t<R> (&a)[1 << NR], const KOp<R>* __restrict__ op) {
-  vec2_t<R> c[8];
-  const vec2_t<R>* mv = reinterpret_cast<const vec2_t<R>*>(op->m);
-  const vec2_t<R>* mrv = reinterpret_cast<const vec2_t<R>*>(op->mr);
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    c[2 * i] = __ldg(mv + i);
-    c[2 * i + 1] = __ldg(mrv + i);
-  }
+__device__ __forceinline__ void mat_full_c(vec2_t<R> (&a)[1 << NR], const vec2_t<R> (&c)[8]) {
 #pragma unroll
   for (int e = 0; e < (1 << NR); ++e) {
     if ((e >> P) & 1) continue;
@@ -518,29 +518,10 @@ __device__ __forceinline__ void mat_full(vec2_t<R> (&a)[1 << NR], const KOp<R>* 
   }
 }
 
-template <typename R, int NR, int P>
-__device__ __forceinline__ void swap_slot(vec2_t<R> (&a)[1 << NR]) {
-#pragma unroll
-  for (int e = 0; e < (1 << NR); ++e) {
-    if ((e >> P) & 1) continue;
-    const vec2_t<R> t = a[e];
-    a[e] = a[e | (1 << P)];
-    a[e | (1 << P)] = t;
-  }
-}
-
 // dense 2x2 on slot P restricted to the pairs whose register slot Q == V
 template <typename R, int NR, int P, int Q, int V>
-__device__ __forceinline__ void mat_q(vec2_t<R> (&a)[1 << NR], const KOp<R>* __restrict__ op) {
+__device__ __forceinline__ void mat_q_c(vec2_t<R> (&a)[1 << NR], const vec2_t<R> (&c)[8]) {
   if constexpr (P < NR && Q < NR && P != Q) {
-    vec2_t<R> c[8];
-    const vec2_t<R>* mv = reinterpret_cast<const vec2_t<R>*>(op->m);
-    const vec2_t<R>* mrv = reinterpret_cast<const vec2_t<R>*>(op->mr);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      c[2 * i] = __ldg(mv + i);
-      c[2 * i + 1] = __ldg(mrv + i);
-    }
 #pragma unroll
     for (int e = 0; e < (1 << NR); ++e) {
       if (((e >> P) & 1) || ((e >> Q) & 1) != V) continue;
@@ -553,70 +534,335 @@ __device__ __forceinline__ void mat_q(vec2_t<R> (&a)[1 << NR], const KOp<R>* __r
   }
 }
 
+__device__ __forceinline__ void swap_bits(float& a, float& b, uint64_t m) {
+  const uint32_t x = __float_as_uint(a), y = __float_as_uint(b), t = (x ^ y) & (uint32_t)m;
+  a = __uint_as_float(x ^ t);
+  b = __uint_as_float(y ^ t);
+}
+__device__ __forceinline__ void swap_bits(double& a, double& b, uint64_t m) {
+  const uint64_t x = (uint64_t)__double_as_longlong(a), y = (uint64_t)__double_as_longlong(b), t = (x ^ y) & m;
+  a = __longlong_as_double((long long)(x ^ t));
+  b = __longlong_as_double((long long)(y ^ t));
+}
+
+// register swap as selects in place (no loop-carried register renaming:
+// a branchy swap made nvcc hoist 32 copies into every op's dispatch)
 template <typename R, int NR, int P, int Q, int V>
-__device__ __forceinline__ void swap_q(vec2_t<R> (&a)[1 << NR]) {
-  if constexpr (P < NR && Q < NR && P != Q) {
+__device__ __forceinline__ void swap_sel(vec2_t<R> (&a)[1 << NR], bool p) {
+  const uint64_t m = p ? ~0ull : 0ull;
+  if constexpr (P < NR && (Q < 0 || (Q < NR && P != Q))) {
 #pragma unroll
     for (int e = 0; e < (1 << NR); ++e) {
-      if (((e >> P) & 1) || ((e >> Q) & 1) != V) continue;
-      const vec2_t<R> t = a[e];
-      a[e] = a[e | (1 << P)];
-      a[e | (1 << P)] = t;
+      if (((e >> P) & 1) || (Q >= 0 && ((e >> Q) & 1) != V)) continue;
+      const int e1 = e | (1 << P);
+      // masked XOR swap: t = (a ^ b) & m, a ^= t, b ^= t (three LOP3, no copies)
+      swap_bits(a[e].x, a[e1].x, m);
+      swap_bits(a[e].y, a[e1].y, m);
     }
   }
 }
 
-// the fast-path op set (every op of the random-circuit workloads): returns
-// false for OPC_GENERIC so the caller can interpret it
-template <typename R, int NR>
-__device__ __forceinline__ bool fast_op(const KOp<R>* __restrict__ op, uint32_t opc, vec2_t<R> (&a)[1 << NR],
-                                        uint64_t gthr) {
-  switch (opc) {
-#define SK_FM(P)                                                                              \
-  case OPC_MAT + P:                                                                           \
-    if (P < NR) mat_full<R, NR, (P < NR ? P : 0)>(a, op);                                     \
-    return true;                                                                              \
-  case OPC_MATT + P:                                                                          \
-    if (P < NR && (gthr & op->tmask) == op->tval) mat_full<R, NR, (P < NR ? P : 0)>(a, op); \
-    return true;                                                                              \
-  case OPC_SWAPT + P:                                                                         \
-    if (P < NR && (gthr & op->tmask) == op->tval) swap_slot<R, NR, (P < NR ? P : 0)>(a);    \
-    return true;
-    SK_FM(0) SK_FM(1) SK_FM(2) SK_FM(3)
-#undef SK_FM
-#define SK_FQ(P, Q, V)                                                                  \
-  case OPC_MATQ + 2 * (4 * P + Q) + V:                                                  \
-    if ((gthr & op->tmask) == op->tval) mat_q<R, NR, P, Q, V>(a, op);                   \
-    return true;                                                                        \
-  case OPC_SWAPQ + 2 * (4 * P + Q) + V:                                                 \
-    if ((gthr & op->tmask) == op->tval) swap_q<R, NR, P, Q, V>(a);                      \
-    return true;
-#define SK_FQ2(P, Q) SK_FQ(P, Q, 0) SK_FQ(P, Q, 1)
-    SK_FQ2(0, 1) SK_FQ2(0, 2) SK_FQ2(0, 3) SK_FQ2(1, 0) SK_FQ2(1, 2) SK_FQ2(1, 3)
-    SK_FQ2(2, 0) SK_FQ2(2, 1) SK_FQ2(2, 3) SK_FQ2(3, 0) SK_FQ2(3, 1) SK_FQ2(3, 2)
-#undef SK_FQ2
-#undef SK_FQ
-    case OPC_PHASE: {
-      if ((gthr & op->tmask) != op->tval) return true;
-      const vec2_t<R> c0 = __ldg(reinterpret_cast<const vec2_t<R>*>(op->m));
-      const vec2_t<R> c1 = __ldg(reinterpret_cast<const vec2_t<R>*>(op->m) + 1);
-      const vec2_t<R> c = (gthr & op->qmask) ? c1 : c0;
-      phase_dispatch<R, NR>(op->h.pat, a, c);
-      return true;
-    }
-    default:
-      return false;
+template <typename R>
+struct SignBit;
+template <>
+struct SignBit<float> {
+  static constexpr uint64_t value = 0x80000000ull;
+};
+template <>
+struct SignBit<double> {
+  static constexpr uint64_t value = 0x8000000000000000ull;
+};
+
+__device__ __forceinline__ float flip_bits(float x, uint64_t m) { return __uint_as_float(__float_as_uint(x) ^ (uint32_t)m); }
+__device__ __forceinline__ double flip_bits(double x, uint64_t m) {
+  return __longlong_as_double(__double_as_longlong(x) ^ (long long)m);
+}
+
+// a[e] = -a[e] on the pattern's elements when m is the sign bit (m = 0: no-op)
+template <typename R, int NR, int P, int VP, int Q, int VQ>
+__device__ __forceinline__ void sign_pat(vec2_t<R> (&a)[1 << NR], uint64_t m) {
+  if constexpr (P < NR && Q < NR) {
+#pragma unroll
+    for (int e = 0; e < (1 << NR); ++e)
+      if (pat_hit<NR, P, VP, Q, VQ>(e)) a[e] = mk<R>(flip_bits(a[e].x, m), flip_bits(a[e].y, m));
   }
+}
+
+#define SK_SIGN_PAIR(P, Q, IDX)                                         \
+  case 9 + 4 * IDX + 0: sign_pat<R, NR, P, 0, Q, 0>(a, m); return;     \
+  case 9 + 4 * IDX + 1: sign_pat<R, NR, P, 0, Q, 1>(a, m); return;     \
+  case 9 + 4 * IDX + 2: sign_pat<R, NR, P, 1, Q, 0>(a, m); return;     \
+  case 9 + 4 * IDX + 3: sign_pat<R, NR, P, 1, Q, 1>(a, m); return;
+
+template <typename R, int NR>
+__device__ __forceinline__ void sign_dispatch(int pat, vec2_t<R> (&a)[1 << NR], uint64_t m) {
+  switch (pat) {
+    case 0: sign_pat<R, NR, -1, 0, -1, 0>(a, m); return;
+    case 1: sign_pat<R, NR, 0, 0, -1, 0>(a, m); return;
+    case 2: sign_pat<R, NR, 0, 1, -1, 0>(a, m); return;
+    case 3: sign_pat<R, NR, 1, 0, -1, 0>(a, m); return;
+    case 4: sign_pat<R, NR, 1, 1, -1, 0>(a, m); return;
+    case 5: sign_pat<R, NR, 2, 0, -1, 0>(a, m); return;
+    case 6: sign_pat<R, NR, 2, 1, -1, 0>(a, m); return;
+    case 7: sign_pat<R, NR, 3, 0, -1, 0>(a, m); return;
+    case 8: sign_pat<R, NR, 3, 1, -1, 0>(a, m); return;
+    SK_SIGN_PAIR(0, 1, 0)
+    SK_SIGN_PAIR(0, 2, 1)
+    SK_SIGN_PAIR(0, 3, 2)
+    SK_SIGN_PAIR(1, 2, 3)
+    SK_SIGN_PAIR(1, 3, 4)
+    SK_SIGN_PAIR(2, 3, 5)
+    default: return;
+  }
+}
+#undef SK_SIGN_PAIR
+
+// Y on slot P (pairs with register slot Q == V; Q < 0: all pairs) when p:
+// y0 = -i a1 = (a1.y, -a1.x), y1 = i a0 = (-a0.y, a0.x) as masked swaps of
+// a0.x <-> a1.y and a0.y <-> a1.x plus two masked sign flips
+template <typename R, int NR, int P, int Q, int V>
+__device__ __forceinline__ void yswap_sel(vec2_t<R> (&a)[1 << NR], bool p) {
+  if constexpr (P < NR && (Q < 0 || (Q < NR && P != Q))) {
+    const uint64_t m = p ? ~0ull : 0ull, sb = p ? SignBit<R>::value : 0ull;
+#pragma unroll
+    for (int e = 0; e < (1 << NR); ++e) {
+      if (((e >> P) & 1) || (Q >= 0 && ((e >> Q) & 1) != V)) continue;
+      const int e1 = e | (1 << P);
+      R a0x = a[e].x, a0y = a[e].y, a1x = a[e1].x, a1y = a[e1].y;
+      swap_bits(a0x, a1y, m);
+      swap_bits(a0y, a1x, m);
+      a[e] = mk<R>(a0x, flip_bits(a0y, sb));
+      a[e1] = mk<R>(flip_bits(a1x, sb), a1y);
+    }
+  }
+}
+
+// real 2x2 on slot P: y0 = m00 a0 + m01 a1, y1 = m10 a0 + m11 a1 (2 paired
+// instructions per output in fp32, half the dense 2x2)
+template <typename R, int NR, int P>
+__device__ __forceinline__ void matr_full_c(vec2_t<R> (&a)[1 << NR], const vec2_t<R> (&c)[8]) {
+  matr_slot<R, NR, P>(a, c[0].x, c[2].x, c[4].x, c[6].x, PairMask<NR, P>::value());
+}
+
+// A LEAN sweep's ops travel in the kernel's parameter space (LSweep, up to
+// kLeanOps ops): warp-uniform constant-bank operands, so coefficients are
+// LDCU loads into uniform registers read directly by FFMA2/FMUL2 — no vector
+// registers, no LSU traffic and a short dispatch chain per op.
+template <typename R>
+struct alignas(16) LOp {
+  KHdr h;
+  uint64_t tmask, tval;  // thread-side predicate
+  uint64_t qmask, pad;   // K_PHASE: c1 when (gthr & qmask) != 0
+  R m[8];                // 2x2 (or phase c0 = m[0..1], c1 = m[2..3])
+  R mr[8];               // m rotated by i per entry
+};
+constexpr int kLeanOps = 128;
+
+template <typename R>
+struct LSweep {
+  DSweep d;  // op_begin / op_end index op[]
+  LOp<R> op[kLeanOps];
+};
+
+template <typename R>
+__device__ __forceinline__ void coefs_of(const LOp<R>& op, vec2_t<R> (&c)[8]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    c[2 * i] = mk<R>(op.m[2 * i], op.m[2 * i + 1]);
+    c[2 * i + 1] = mk<R>(op.mr[2 * i], op.mr[2 * i + 1]);
+  }
+}
+
+// thread-predicated 2x2: the identity where the predicate fails (selects, no
+// divergent exit: the op loop stays warp-uniform so its indices and
+// coefficients live in uniform registers)
+template <typename R>
+__device__ __forceinline__ void coefs_if(const LOp<R>& op, vec2_t<R> (&c)[8], bool p) {
+  coefs_of<R>(op, c);
+  const R one = 1, zero = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const bool diag = i == 0 || i == 1 || i == 6 || i == 7;  // m00, r00, m11, r11
+    const bool rot = i & 1;                                   // identity r = (0, 1)
+    const R ix = diag && !rot ? one : zero, iy = diag && rot ? one : zero;
+    c[i] = mk<R>(p ? c[i].x : ix, p ? c[i].y : iy);
+  }
+}
+
+// [[c, -s w], [s, c w]] on slot P (c, s real, |w| = 1; split_1q's gates):
+// t = w a1 (w and its rotation wr = (-w.y, w.x) as packed operands), then
+// y0 = c a0 - s t, y1 = s a0 + c t: 6 paired instructions per pair, not 8
+template <typename R, int NR, int P>
+__device__ __forceinline__ void matrp_slot(vec2_t<R> (&a)[1 << NR], R c, R s, vec2_t<R> w, vec2_t<R> wr) {
+  if constexpr (P < NR) {
+#pragma unroll
+    for (int e = 0; e < (1 << NR); ++e) {
+      if ((e >> P) & 1) continue;
+      const int e1 = e | (1 << P);
+      const vec2_t<R> x0 = a[e], x1 = a[e1];
+      if constexpr (sizeof(R) == 4) {
+        const float2 t = __ffma2_rn(make_float2(x1.y, x1.y), wr, __fmul2_rn(make_float2(x1.x, x1.x), w));
+        a[e] = __ffma2_rn(t, make_float2(-s, -s), __fmul2_rn(x0, make_float2(c, c)));
+        a[e1] = __ffma2_rn(t, make_float2(c, c), __fmul2_rn(x0, make_float2(s, s)));
+      } else {
+        const vec2_t<R> t = mk<R>(x1.x * w.x - x1.y * w.y, x1.x * w.y + x1.y * w.x);
+        a[e] = mk<R>(c * x0.x - s * t.x, c * x0.y - s * t.y);
+        a[e1] = mk<R>(s * x0.x + c * t.x, s * x0.y + c * t.y);
+      }
+    }
+  }
+}
+
+template <typename R, int NR, int P, int V>
+__device__ __forceinline__ void phase_slot(vec2_t<R> (&a)[1 << NR], vec2_t<R> c) {
+  if constexpr (P < NR) {
+#pragma unroll
+    for (int e = 0; e < (1 << NR); ++e)
+      if (((e >> P) & 1) == V) a[e] = PK<R>::mul(a[e], c);
+  }
+}
+
+// compile-time dispatch of a warp-uniform index by binary search: nested
+// two-way branches stay uniform (BRA.U), where a large switch becomes a
+// jump table whose indirect branch pushes the whole op loop (index,
+// coefficients) out of the uniform datapath
+template <int LO, int HI, typename F>
+__device__ __forceinline__ void sel(int i, F&& f) {
+  if constexpr (HI - LO == 1) {
+    f(std::integral_constant<int, LO>{});
+  } else {
+    constexpr int MID = (LO + HI) / 2;
+    if (i < MID)
+      sel<LO, MID>(i, f);
+    else
+      sel<MID, HI>(i, f);
+  }
+}
+
+// phase / sign pattern codes (host pattern_of agrees): 0 = all elements;
+// 1 + 2P + VP = slot P == VP; 9 + 4 pair(P<Q) + 2VP + VQ = both conditions
+struct PatCode {
+  int p, vp, q, vq;
+};
+__host__ __device__ constexpr PatCode pat_code(int k) {
+  constexpr int pp[6] = {0, 0, 0, 1, 1, 2}, qq[6] = {1, 2, 3, 2, 3, 3};
+  return k == 0 ? PatCode{-1, 0, -1, 0}
+       : k <= 8 ? PatCode{(k - 1) / 2, (k - 1) % 2, -1, 0}
+                : PatCode{pp[(k - 9) / 4], ((k - 9) / 2) % 2, qq[(k - 9) / 4], (k - 9) % 2};
+}
+
+// LEAN dispatch: one uniform branch tree per op (opcode ranges, then the
+// slot / pattern index); thread predicates are selects, never exits
+template <typename R, int NR>
+__device__ __forceinline__ void lean_op(const LOp<R>& op, uint32_t opc, vec2_t<R> (&a)[1 << NR], uint64_t gthr) {
+  const int o = (int)opc;
+  if (o < OPC_MATT) {  // unpredicated dense 2x2: most ops of a random circuit
+    vec2_t<R> c[8];
+    coefs_of<R>(op, c);
+    sel<0, 4>(o - OPC_MAT, [&](auto k) {
+      constexpr int P = decltype(k)::value;
+      if constexpr (P < NR) mat_full_c<R, NR, P>(a, c);
+    });
+    return;
+  }
+  if (o >= OPC_MATR && o < OPC_DIAG1) {  // real 2x2 (split 1q gates)
+    vec2_t<R> c[8];
+    coefs_of<R>(op, c);
+    sel<0, 4>(o - OPC_MATR, [&](auto k) {
+      constexpr int P = decltype(k)::value;
+      if constexpr (P < NR) matr_full_c<R, NR, P>(a, c);
+    });
+    return;
+  }
+  if (o >= OPC_MATRP) {  // real first column (split 1q gates): m = c, s; mr = w, wr
+    const R c = op.m[0], sn = op.m[4];
+    const vec2_t<R> w = mk<R>(op.mr[0], op.mr[1]), wr = mk<R>(op.mr[2], op.mr[3]);
+    sel<0, 4>(o - OPC_MATRP, [&](auto k) { matrp_slot<R, NR, decltype(k)::value>(a, c, sn, w, wr); });
+    return;
+  }
+  if (o >= OPC_DIAG1 && o < OPC_MATRP) {  // phase on one slot value
+    const vec2_t<R> c = mk<R>(op.m[0], op.m[1]);
+    sel<0, 8>(o - OPC_DIAG1, [&](auto k) {
+      constexpr int K = decltype(k)::value;
+      phase_slot<R, NR, K / 2, K % 2>(a, c);
+    });
+    return;
+  }
+  const bool p = (gthr & op.tmask) == op.tval;
+  if (o < OPC_SWAPT) {  // OPC_MATT: dense 2x2 behind a thread predicate
+    vec2_t<R> c[8];
+    coefs_if<R>(op, c, p);
+    sel<0, 4>(o - OPC_MATT, [&](auto k) {
+      constexpr int P = decltype(k)::value;
+      if constexpr (P < NR) mat_full_c<R, NR, P>(a, c);
+    });
+    return;
+  }
+  if (o < OPC_MATQ) {  // OPC_SWAPT: X on a slot
+    sel<0, 4>(o - OPC_SWAPT, [&](auto k) { swap_sel<R, NR, decltype(k)::value, -1, 0>(a, p); });
+    return;
+  }
+  if (o < OPC_SWAPQ) {  // OPC_MATQ: dense 2x2 on pairs with slot Q == V
+    vec2_t<R> c[8];
+    coefs_if<R>(op, c, p);
+    sel<0, 32>(o - OPC_MATQ, [&](auto k) {
+      constexpr int K = decltype(k)::value;
+      mat_q_c<R, NR, K / 8, (K / 2) % 4, K % 2>(a, c);
+    });
+    return;
+  }
+  if (o < OPC_PHASE) {  // OPC_SWAPQ
+    sel<0, 32>(o - OPC_SWAPQ, [&](auto k) {
+      constexpr int K = decltype(k)::value;
+      swap_sel<R, NR, K / 8, (K / 2) % 4, K % 2>(a, p);
+    });
+    return;
+  }
+  if (o == OPC_PHASE) {  // general phase: selected multiplier per element
+    const vec2_t<R> c = (gthr & op.qmask) ? mk<R>(op.m[2], op.m[3]) : mk<R>(op.m[0], op.m[1]);
+    const uint32_t em = p ? op.h.emask : 0u;
+#pragma unroll
+    for (int e = 0; e < (1 << NR); ++e) {
+      const bool hit = (em >> e) & 1u;
+      a[e] = PK<R>::mul(a[e], mk<R>(hit ? c.x : (R)1, hit ? c.y : (R)0));
+    }
+    return;
+  }
+  if (o == OPC_SIGN) {  // by -1: sign-bit flips
+    const bool ps = p && (op.qmask == 0 || (gthr & op.qmask) != 0);
+    const uint64_t m = ps ? SignBit<R>::value : 0ull;
+    sel<0, 33>(op.h.pat, [&](auto k) {
+      constexpr PatCode pc = pat_code(decltype(k)::value);
+      sign_pat<R, NR, pc.p, pc.vp, pc.q, pc.vq>(a, m);
+    });
+    return;
+  }
+  if (o < OPC_YSWAPQ) {  // OPC_YSWAPT
+    sel<0, 4>(o - OPC_YSWAPT, [&](auto k) { yswap_sel<R, NR, decltype(k)::value, -1, 0>(a, p); });
+    return;
+  }
+  sel<0, 32>(o - OPC_YSWAPQ, [&](auto k) {  // OPC_YSWAPQ
+    constexpr int K = decltype(k)::value;
+    yswap_sel<R, NR, K / 8, (K / 2) % 4, K % 2>(a, p);
+  });
 }
 
 // Generic fused sweep (random circuits, mixed gate streams): NS compile-time
 // stages with per-thread index parts from the host-built table `thr`
 // (uint4 per stage and thread: global bits lo/hi, swizzled shared offset),
 // ops interpreted from `ops` with warp-uniform loads and packed arithmetic.
+__device__ __forceinline__ const DSweep& dsweep_of(const DSweep& s) { return s; }
+template <typename R>
+__device__ __forceinline__ const DSweep& dsweep_of(const LSweep<R>& s) { return s.d; }
+
+template <typename R, bool LEAN>
+using SweepArg = std::conditional_t<LEAN, LSweep<R>, DSweep>;
+
 template <typename R, int NR, int NS, bool LEAN>
-__global__ void __launch_bounds__(512, 1) k_sweep(vec2_t<R>* __restrict__ amps, const __grid_constant__ DSweep sw,
+__global__ void k_sweep(vec2_t<R>* __restrict__ amps, const __grid_constant__ SweepArg<R, LEAN> arg,
                                                   const KOp<R>* __restrict__ ops, const uint4* __restrict__ thr) {
   using V = vec2_t<R>;
+  const DSweep& sw = dsweep_of(arg);
   extern __shared__ __align__(16) unsigned char smraw[];
   constexpr int NE = 1 << NR;
   const uint32_t tid = threadIdx.x;
@@ -624,8 +870,8 @@ __global__ void __launch_bounds__(512, 1) k_sweep(vec2_t<R>* __restrict__ amps, 
   const int nthreads = blockDim.x;
 
   V a[NE];
-#pragma unroll
-  for (int s = 0; s < NS; ++s) {
+#pragma unroll 1
+  for (int s = 0; s < NS; ++s) {  // not unrolled: one copy of the op loop (its uniform index) per kernel
     const DStage& st = sw.st[s];
     const uint4 t = __ldg(thr + s * nthreads + tid);
     const uint64_t gthr = base | ((uint64_t)t.y << 32 | t.x);
@@ -651,7 +897,10 @@ __global__ void __launch_bounds__(512, 1) k_sweep(vec2_t<R>* __restrict__ amps, 
       }
     }
     if constexpr (LEAN) {  // every op of the sweep has a fast path: no interpreter in the loop
-      for (int o = st.op_begin; o < st.op_end; ++o) fast_op<R, NR>(ops + o, ops[o].h.opc, a, gthr);
+      // warp reductions mark the op range warp-uniform (the stage loop is not
+      // unrolled, so nvcc would otherwise index the op table from vector
+      // registers): op fields then load with LDCU into uniform registers
+      for (int o = st.op_begin; o < st.op_end; ++o) lean_op<R, NR>(arg.op[o], arg.op[o].h.opc, a, gthr);
     } else {
       // sweeps with ops outside the fast-path set are interpreted op by op
       // (inlining the fast-path table here too multiplied nvcc time)
@@ -1258,17 +1507,36 @@ static int lower_op(const StageCtx& c, const sk_op& op, int o, int width, std::v
 
 static uint32_t opcode_of(const HostKOp& k) {
   if (k.nr > 4) return OPC_GENERIC;
-  if (k.kind == K_PHASE && k.pat >= 0 && !(k.flags & ~(uint32_t)(F_TPRED | F_QMASK))) return OPC_PHASE;
+  if (k.kind == K_PHASE && k.pat >= 0 && !(k.flags & ~(uint32_t)(F_TPRED | F_QMASK))) {
+    // by -1 (CZ-type couplers): sign flips instead of complex multiplies
+    const bool q = (k.flags & F_QMASK) != 0;
+    if (k.m[2] == -1 && k.m[3] == 0 && k.m[1] == 0 && k.m[0] == (q ? 1 : -1)) return OPC_SIGN;
+    if (k.flags == 0 && k.pat >= 1 && k.pat <= 8) return OPC_DIAG1 + (k.pat - 1);  // one slot condition
+    return OPC_PHASE;
+  }
   if (k.slot < 0 || k.slot >= k.nr || (k.flags & ~(uint32_t)F_TPRED)) return OPC_GENERIC;
   const bool swap = k.kind == K_MATR && k.m[0] == 0 && k.m[2] == 1 && k.m[4] == 1 && k.m[6] == 0;
+  const bool ymat = k.kind == K_MAT && k.m[0] == 0 && k.m[1] == 0 && k.m[2] == 0 && k.m[3] == -1 && k.m[4] == 0 &&
+                    k.m[5] == 1 && k.m[6] == 0 && k.m[7] == 0;
+  if (k.kind == K_MATR && !swap && k.tmask == 0 && k.emask == slot_mask(k.nr, k.slot, 0)) return OPC_MATR + k.slot;
+  if (k.kind == K_MAT && k.m[1] == 0 && k.m[5] == 0 && k.m[0] >= 0 && k.m[4] >= 0 && k.tmask == 0 &&
+      k.emask == slot_mask(k.nr, k.slot, 0) && !(k.flags & ~(uint32_t)F_TPRED) && (k.m[0] > 0 || k.m[4] > 0)) {
+    // [[c, -s w], [s, c w]] (see lean_param) only when the matrix has exactly that form
+    const double c = k.m[0], sn = k.m[4];
+    const double wx = c >= sn ? k.m[6] / c : -k.m[2] / sn, wy = c >= sn ? k.m[7] / c : -k.m[3] / sn;
+    const double e = std::fabs(k.m[2] + sn * wx) + std::fabs(k.m[3] + sn * wy) + std::fabs(k.m[6] - c * wx) +
+                     std::fabs(k.m[7] - c * wy) + std::fabs(wx * wx + wy * wy - 1.0);
+    if (e < 1e-13) return OPC_MATRP + k.slot;
+  }
   if (k.kind != K_MAT && !swap) return OPC_GENERIC;
   const bool tp = (k.flags & F_TPRED) != 0;
   const uint32_t full = slot_mask(k.nr, k.slot, 0);
-  if (k.emask == full) return swap ? OPC_SWAPT + k.slot : (tp ? OPC_MATT : OPC_MAT) + k.slot;
+  if (k.emask == full)
+    return swap ? OPC_SWAPT + k.slot : ymat ? OPC_YSWAPT + k.slot : (tp ? OPC_MATT : OPC_MAT) + k.slot;
   for (int q = 0; q < k.nr; ++q)  // one register-side control
     for (int v = 0; v < 2; ++v)
       if (q != k.slot && k.emask == (full & slot_mask(k.nr, q, v)))
-        return (swap ? OPC_SWAPQ : OPC_MATQ) + 2 * (4 * k.slot + q) + v;
+        return (swap ? OPC_SWAPQ : ymat ? OPC_YSWAPQ : OPC_MATQ) + 2 * (4 * k.slot + q) + v;
   return OPC_GENERIC;
 }
 
@@ -1299,6 +1567,51 @@ static void pack_kops(std::vector<HostKOp>& h, std::vector<unsigned char>& buf) 
     }
     for (int j = 0; j < 16; ++j) x.tw[j] = (R)h[i].tw[j];
     k[i] = x;
+  }
+}
+
+// the LEAN kernel's parameter block of one sweep: its DSweep with op indices
+// rebased onto the sweep's own ops, copied out of the packed KOp array
+template <typename R>
+static void lean_param(const DSweep& d, const std::vector<unsigned char>& buf, std::vector<unsigned char>& out) {
+  out.clear();
+  if (!d.lean || d.nstages < 1) return;
+  const int first = d.st[0].op_begin, last = d.st[d.nstages - 1].op_end;
+  if (last - first > kLeanOps) return;  // too many ops for the parameter space: generic kernel
+  static_assert(sizeof(LSweep<R>) + 3 * sizeof(void*) <= 32764, "LSweep exceeds the kernel parameter space");
+  out.assign(sizeof(LSweep<R>), 0);
+  LSweep<R>* ls = reinterpret_cast<LSweep<R>*>(out.data());
+  ls->d = d;
+  for (int s = 0; s < d.nstages; ++s) {
+    ls->d.st[s].op_begin -= first;
+    ls->d.st[s].op_end -= first;
+  }
+  const KOp<R>* k = reinterpret_cast<const KOp<R>*>(buf.data());
+  for (int o = first; o < last; ++o) {
+    LOp<R>& x = ls->op[o - first];
+    x.h = k[o].h;
+    x.tmask = k[o].tmask;
+    x.tval = k[o].tval;
+    x.qmask = k[o].qmask;
+    for (int j = 0; j < 8; ++j) {
+      x.m[j] = k[o].m[j];
+      x.mr[j] = k[o].mr[j];
+    }
+    if (x.h.opc >= OPC_MATRP && x.h.opc < OPC_END) {  // m = (c, s) at m[0], m[4]; mr = w, (-w.y, w.x)
+      const double c = (double)k[o].m[0], sn = (double)k[o].m[4];
+      double wx, wy;
+      if (c >= sn) {
+        wx = (double)k[o].m[6] / c;
+        wy = (double)k[o].m[7] / c;
+      } else {
+        wx = -(double)k[o].m[2] / sn;
+        wy = -(double)k[o].m[3] / sn;
+      }
+      x.mr[0] = (R)wx;
+      x.mr[1] = (R)wy;
+      x.mr[2] = (R)-wy;
+      x.mr[3] = (R)wx;
+    }
   }
 }
 
@@ -1418,6 +1731,7 @@ struct sk_program {
   uint64_t pconst = 0;
   void* d_ops = nullptr;
   int nkops = 0;
+  std::vector<std::vector<unsigned char>> lean;  // per sweep: LSweep<R> bytes (empty: not a LEAN sweep)
 };
 
 using namespace sk;
@@ -1469,15 +1783,19 @@ static int launch_one(sk_state* s, const sk_program* p, int i, DevCtx* c, int64_
   if (!attr_set[s->device]) {
 #define SK_ATTR(K) SK_CUDA(cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024))
     if constexpr (NR <= 4 && !(sizeof(R) == 8 && NR == 4)) {
+#ifndef SK_DEV_SWEEP_ONLY
       SK_ATTR((k_sweep<R, NR, 1, false>)); SK_ATTR((k_sweep<R, NR, 2, false>)); SK_ATTR((k_sweep<R, NR, 3, false>));
       SK_ATTR((k_sweep<R, NR, 4, false>)); SK_ATTR((k_sweep<R, NR, 5, false>)); SK_ATTR((k_sweep<R, NR, 6, false>));
       SK_ATTR((k_sweep<R, NR, 7, false>)); SK_ATTR((k_sweep<R, NR, 8, false>));
+#endif
       SK_ATTR((k_sweep<R, NR, 1, true>)); SK_ATTR((k_sweep<R, NR, 2, true>)); SK_ATTR((k_sweep<R, NR, 3, true>));
       SK_ATTR((k_sweep<R, NR, 4, true>)); SK_ATTR((k_sweep<R, NR, 5, true>)); SK_ATTR((k_sweep<R, NR, 6, true>));
       SK_ATTR((k_sweep<R, NR, 7, true>)); SK_ATTR((k_sweep<R, NR, 8, true>));
     }
+#ifndef SK_DEV_SWEEP_ONLY
     SK_ATTR((k_qft<R, NR, 1>)); SK_ATTR((k_qft<R, NR, 2>)); SK_ATTR((k_qft<R, NR, 3>));
     SK_ATTR((k_qft<R, NR, 4>)); SK_ATTR((k_qft<R, NR, 5>)); SK_ATTR((k_qft<R, NR, 6>));
+#endif
 #undef SK_ATTR
     attr_set[s->device] = true;
   }
@@ -1495,6 +1813,7 @@ static int launch_one(sk_state* s, const sk_program* p, int i, DevCtx* c, int64_
   vec2_t<R>* d_amps = (vec2_t<R>*)s->d;
   // 5-bit c64 and 4-bit c128 sweeps exist only as QFT windows: SK_QFT_KERNEL=0 cannot route them elsewhere
   constexpr bool qft_only = NR > 4 || (sizeof(R) == 8 && NR == 4);
+#ifndef SK_DEV_SWEEP_ONLY
   if (p->qft_ok[i] && threads <= (unsigned)qft_max_threads<R, NR>() && (qft_only || use_qft_kernel())) {
     QSweep q = p->pshift ? phase_shifted(p->qsweeps[i], p->pshift, p->pconst) : p->qsweeps[i];
     q.tile0 = (int)tb;
@@ -1507,7 +1826,9 @@ static int launch_one(sk_state* s, const sk_program* p, int i, DevCtx* c, int64_
 #undef SK_QS
       default: return set_error(SK_EVALUE, "sweep %d: %d stages", i, q.nstages);
     }
-  } else if (tb != 0 || te != (int64_t)all_tiles) {
+  } else
+#endif
+  if (tb != 0 || te != (int64_t)all_tiles) {
     return set_error(SK_EVALUE, "sweep %d: tile ranges need the QFT-window kernel", i);
   } else if constexpr (NR > 4 || (sizeof(R) == 8 && NR == 4)) {  // 4-bit c128 / 5-bit c64: QFT windows only
     return set_error(SK_EVALUE, "sweep %d: %d register bits need the QFT-window kernel", i, NR);
@@ -1516,14 +1837,22 @@ static int launch_one(sk_state* s, const sk_program* p, int i, DevCtx* c, int64_
   } else {
     const KOp<R>* ops = (const KOp<R>*)p->d_ops;
     const uint4* thr = (const uint4*)p->d_thr + p->thr_off[i];
-    switch (d.nstages * 2 + (d.lean && use_lean_kernel() ? 1 : 0)) {
+    const bool lean = !p->lean[i].empty() && use_lean_kernel();
+    const LSweep<R>* ls = lean ? reinterpret_cast<const LSweep<R>*>(p->lean[i].data()) : nullptr;
+    switch (d.nstages * 2 + (lean ? 1 : 0)) {
+#ifdef SK_DEV_SWEEP_ONLY
+#define SK_GENERIC_SWEEP(NS_) return set_error(SK_EVALUE, "development build: LEAN sweeps only");
+#else
+#define SK_GENERIC_SWEEP(NS_) \
+  k_sweep<R, NR, NS_, false><<<(unsigned)tiles, threads, smem, c->stream>>>(d_amps, d, ops, thr); break;
+#endif
 #define SK_GS(NS_)                                                                                          \
-  case 2 * NS_: k_sweep<R, NR, NS_, false><<<(unsigned)tiles, threads, smem, c->stream>>>(d_amps, d, ops, thr); \
-    break;                                                                                                  \
-  case 2 * NS_ + 1: k_sweep<R, NR, NS_, true><<<(unsigned)tiles, threads, smem, c->stream>>>(d_amps, d, ops, thr); \
+  case 2 * NS_: SK_GENERIC_SWEEP(NS_)                                                                       \
+  case 2 * NS_ + 1: k_sweep<R, NR, NS_, true><<<(unsigned)tiles, threads, smem, c->stream>>>(d_amps, *ls, ops, thr); \
     break;
       SK_GS(1) SK_GS(2) SK_GS(3) SK_GS(4) SK_GS(5) SK_GS(6) SK_GS(7) SK_GS(8)
 #undef SK_GS
+#undef SK_GENERIC_SWEEP
       default: return set_error(SK_EVALUE, "sweep %d: %d stages", i, d.nstages);
     }
   }
@@ -1535,6 +1864,11 @@ static int launch_sweeps(sk_state* s, const sk_program* p, int first, int count,
                          int64_t te = -1) {
   for (int i = first; i < first + count; ++i) {
     const int nr = p->sweeps[i].nr;
+#ifdef SK_DEV_SWEEP_ONLY  // fast development build: c64 generic LEAN sweeps only
+    if (s->dtype != SK_C64 || nr != 4) return set_error(SK_EVALUE, "development build: c64 4-bit sweeps only");
+    SK_TRY((launch_one<float, 4>(s, p, i, c, tb, te)));
+    continue;
+#endif
     if (s->dtype == SK_C64 && nr == 5) {
       SK_TRY((launch_one<float, 5>(s, p, i, c, tb, te)));
     } else if (s->dtype == SK_C64) {
@@ -1698,6 +2032,13 @@ int sk_program_create(int width, int dtype, int device, const sk_sweep* sweeps, 
       return set_error(SK_ECUDA, "program upload: %s", cudaGetErrorString(e));
     }
     for (size_t i = 0; i < dsw.size(); ++i) prog->qsweeps[i].thr = (const uint4*)prog->d_thr + prog->thr_off[i];
+  }
+  prog->lean.resize(dsw.size());
+  for (size_t i = 0; i < dsw.size(); ++i) {
+    if (dtype == SK_C64)
+      lean_param<float>(dsw[i], buf, prog->lean[i]);
+    else
+      lean_param<double>(dsw[i], buf, prog->lean[i]);
   }
   prog->sweeps = std::move(dsw);
   prog->nkops = (int)kops.size();

@@ -62,13 +62,14 @@ class Op:
     ctrl_val: int = 0
     nbits: int = 0
     src: int = -1  # index of the originating gate (diagnostics)
+    pin: bool = False  # a phase of split_1q: keep its bit a register bit of its stage
 
     @property
     def tmask(self) -> int:
-        """Bits acted on non-diagonally."""
+        """Bits acted on non-diagonally (and the bit of a pinned phase)."""
         if self.kind == QFT:
             return ((1 << self.nbits) - 1) << self.qubit
-        return (1 << self.qubit) if self.kind == MAT else 0
+        return (1 << self.qubit) if self.kind == MAT or self.pin else 0
 
     @property
     def smask(self) -> int:
@@ -143,6 +144,99 @@ def merge_1q(ops: list[Op]) -> list[Op]:
             if (sm >> bit) & 1:
                 del last[bit]
         out.append(op)
+    return out
+
+
+SPLIT_1Q = bool(int(__import__("os").environ.get("SK_SPLIT_1Q", "1")))
+
+
+def _zyz(m: np.ndarray):
+    """m = e^{i g} diag(1, e^{i a}) [[c, -s], [s, c]] diag(1, e^{i b}) with
+    c = |m00|, s = |m10| (m unitary); returns (g, a, b, c, s)."""
+    c, s = abs(m[0, 0]), abs(m[1, 0])
+    if c > 1e-300:
+        g = cmath.phase(m[0, 0])
+        b = cmath.phase(-m[0, 1]) - g if s > 1e-300 else cmath.phase(m[1, 1]) - g
+        a = cmath.phase(m[1, 0]) - g if s > 1e-300 else 0.0
+    else:  # anti-diagonal: pick g from m10 (a = 0)
+        g = cmath.phase(m[1, 0])
+        a = 0.0
+        b = cmath.phase(-m[0, 1]) - g
+    return g, a, b, c, s
+
+
+def _splittable(op: Op) -> bool:
+    """An uncontrolled dense 1q op that is neither real nor H-like (those keep
+    their own fast paths)."""
+    if op.kind != MAT or op.ctrl_mask:
+        return False
+    real = all(op.m[i] == 0.0 for i in (1, 3, 5, 7))
+    bfly = op.m[0] == op.m[2] and op.m[1] == op.m[3] and op.m[4] == -op.m[6] and op.m[5] == -op.m[7]
+    return not real and not bfly
+
+
+def _mat(op: Op) -> np.ndarray:
+    return np.array([[complex(op.m[0], op.m[1]), complex(op.m[2], op.m[3])],
+                     [complex(op.m[4], op.m[5]), complex(op.m[6], op.m[7])]])
+
+
+def split_1q(ops: list[Op]) -> list[Op]:
+    """Carry the output phase of dense 1q gates to the next dense gate on the
+    same bit.  U = e^{ig} diag(1, e^{ia}) R diag(1, e^{ib}) (R real): when
+    every op between U and the next splittable gate V on that bit is
+    diagonal on it (controlled phases, uses as a control, other bits),
+    diag(1, e^{ia}) commutes up to V, so U is emitted as R diag(1, e^{ib}) —
+    a 2x2 with a real first column, which k_sweep runs as a phase on a1 plus
+    a real rotation (6 paired instructions per pair instead of 8) — and V
+    absorbs the phase into its own input side.  The op count is unchanged;
+    gates without such a successor stay full 2x2s (and carry the global
+    phase).  Exact up to fp64 rounding (the fused-executor tests check it
+    against the oracle)."""
+    n = len(ops)
+    # nxt[i]: for a splittable op i, True when the next op non-diagonal on its
+    # bit is again a splittable op (its deferred phase has a consumer)
+    nxt = [False] * n
+    last: dict[int, int] = {}  # bit -> index of the next op non-diagonal on it (scanning backwards)
+    for i in range(n - 1, -1, -1):
+        op = ops[i]
+        if _splittable(op):
+            j = last.get(op.qubit)
+            nxt[i] = j is not None and _splittable(ops[j])
+        for q in _bits(op.tmask):
+            last[q] = i
+    out: list[Op] = []
+    pend: dict[int, float] = {}
+    gphase = 0.0
+    full_idx = -1
+    for i, op in enumerate(ops):
+        if not _splittable(op):
+            out.append(op)
+            continue
+        q = op.qubit
+        m = _mat(op)
+        if abs(abs(np.linalg.det(m)) - 1.0) > 1e-9 or np.max(np.abs(m.conj().T @ m - np.eye(2))) > 1e-9:
+            m = m @ np.diag([1.0, cmath.exp(1j * pend.pop(q, 0.0))])  # not unitary: dense as given
+            out.append(Op(MAT, q, _m8(m), src=op.src))
+            continue
+        g, a, b, c, s_ = _zyz(m)
+        b += pend.pop(q, 0.0)
+        eb = cmath.exp(1j * b)
+        if nxt[i]:  # R diag(1, e^{ib}); diag(1, e^{ia}) moves on to the next gate on q
+            pend[q] = a
+            gphase += g
+            out.append(Op(MAT, q, (c, 0.0, -s_ * eb.real, -s_ * eb.imag, s_, 0.0, c * eb.real, c * eb.imag),
+                          src=op.src))
+        else:  # the whole gate, with the phases it absorbed
+            mm = cmath.exp(1j * g) * np.array([[c, -s_ * eb], [s_ * cmath.exp(1j * a), c * cmath.exp(1j * a) * eb]])
+            out.append(Op(MAT, q, _m8(mm), src=op.src))
+            full_idx = len(out) - 1
+    assert not pend, "deferred phases must all be consumed"
+    gw = _wrap(gphase)
+    if gw != 0.0:
+        if full_idx < 0:  # cannot happen (the last splittable gate on a bit is always full)
+            raise AssertionError("no full gate to carry the global phase")
+        o = out[full_idx]
+        out[full_idx] = Op(MAT, o.qubit, _m8(cmath.exp(1j * gw) * _mat(o)), src=o.src)
     return out
 
 
@@ -454,6 +548,8 @@ def plan_circuit(circuit: Circuit, dtype: str = "c64", tile_bits: int | None = N
             pass  # geometry the QFT form cannot pad: fall back to generic sweeps
     if fuse:
         ops = merge_1q(ops)
+        if SPLIT_1Q:
+            ops = split_1q(ops)
     return plan_ops(ops, circuit.width, dtype, tile_bits, low_bits, phys, len(circuit.gates))
 
 
