@@ -87,18 +87,16 @@ struct alignas(16) KHdr {
 enum KOpc : uint32_t {
   OPC_GENERIC = 0,
   OPC_MAT = 1,     // + P: dense 2x2 on slot P, unpredicated
-  OPC_MATT = 5,    // + P: same behind a thread-side predicate
-  OPC_SWAPT = 9,   // + P: X on slot P (register swap), optional thread predicate
-  OPC_MATQ = 16,   // + 2 (4P + Q) + V: dense 2x2 on slot P where register slot Q == V
-  OPC_SWAPQ = 48,  // + 2 (4P + Q) + V: X on slot P where register slot Q == V
-  OPC_PHASE = 80,  // K_PHASE with a specialised element pattern
-  OPC_SIGN = 81,   // K_PHASE by -1 (CZ-type couplers): sign-bit flips on the pattern's elements
-  OPC_YSWAPT = 82,  // + P: Y on slot P (swap with +-i: register moves and sign flips), thread predicate
-  OPC_YSWAPQ = 86,  // + 2 (4P + Q) + V: Y on slot P where register slot Q == V
-  OPC_MATR = 118,   // + P: real 2x2 on slot P, unpredicated (the R_y factor of a split 1q gate)
-  OPC_DIAG1 = 122,  // + 2P + V: phase on the elements whose slot P == V, unpredicated
-  OPC_MATRP = 130,  // + P: 2x2 with a real first column = real rotation after a phase on a1
-  OPC_END = 134
+  OPC_MATRP = 5,   // + P: 2x2 with a real first column = real rotation after a phase on a1 (split 1q gates)
+  OPC_MATR = 9,    // + P: real 2x2 on slot P, unpredicated
+  OPC_MATT = 13,   // + P: dense 2x2 behind a thread-side predicate
+  OPC_MATQ = 17,   // + 2 (4P + Q) + V: dense 2x2 on slot P where register slot Q == V
+  OPC_SWAPM = 49,  // + P: X on slot P for the pairs in the element mask, thread predicate
+  OPC_YSWAPM = 53, // + P: Y likewise (swap with +-i: bit moves and sign flips)
+  OPC_SIGNM = 57,  // by -1 (CZ-type couplers) on the elements in the mask: sign-bit flips
+  OPC_DIAG1 = 58,  // + 2P + V: phase on the elements whose slot P == V, unpredicated
+  OPC_PHASE = 66,  // any other K_PHASE: a selected multiplier per element
+  OPC_END = 67
 };
 
 template <typename R>
@@ -545,23 +543,6 @@ __device__ __forceinline__ void swap_bits(double& a, double& b, uint64_t m) {
   b = __longlong_as_double((long long)(y ^ t));
 }
 
-// register swap as selects in place (no loop-carried register renaming:
-// a branchy swap made nvcc hoist 32 copies into every op's dispatch)
-template <typename R, int NR, int P, int Q, int V>
-__device__ __forceinline__ void swap_sel(vec2_t<R> (&a)[1 << NR], bool p) {
-  const uint64_t m = p ? ~0ull : 0ull;
-  if constexpr (P < NR && (Q < 0 || (Q < NR && P != Q))) {
-#pragma unroll
-    for (int e = 0; e < (1 << NR); ++e) {
-      if (((e >> P) & 1) || (Q >= 0 && ((e >> Q) & 1) != V)) continue;
-      const int e1 = e | (1 << P);
-      // masked XOR swap: t = (a ^ b) & m, a ^= t, b ^= t (three LOP3, no copies)
-      swap_bits(a[e].x, a[e1].x, m);
-      swap_bits(a[e].y, a[e1].y, m);
-    }
-  }
-}
-
 template <typename R>
 struct SignBit;
 template <>
@@ -578,64 +559,6 @@ __device__ __forceinline__ double flip_bits(double x, uint64_t m) {
   return __longlong_as_double(__double_as_longlong(x) ^ (long long)m);
 }
 
-// a[e] = -a[e] on the pattern's elements when m is the sign bit (m = 0: no-op)
-template <typename R, int NR, int P, int VP, int Q, int VQ>
-__device__ __forceinline__ void sign_pat(vec2_t<R> (&a)[1 << NR], uint64_t m) {
-  if constexpr (P < NR && Q < NR) {
-#pragma unroll
-    for (int e = 0; e < (1 << NR); ++e)
-      if (pat_hit<NR, P, VP, Q, VQ>(e)) a[e] = mk<R>(flip_bits(a[e].x, m), flip_bits(a[e].y, m));
-  }
-}
-
-#define SK_SIGN_PAIR(P, Q, IDX)                                         \
-  case 9 + 4 * IDX + 0: sign_pat<R, NR, P, 0, Q, 0>(a, m); return;     \
-  case 9 + 4 * IDX + 1: sign_pat<R, NR, P, 0, Q, 1>(a, m); return;     \
-  case 9 + 4 * IDX + 2: sign_pat<R, NR, P, 1, Q, 0>(a, m); return;     \
-  case 9 + 4 * IDX + 3: sign_pat<R, NR, P, 1, Q, 1>(a, m); return;
-
-template <typename R, int NR>
-__device__ __forceinline__ void sign_dispatch(int pat, vec2_t<R> (&a)[1 << NR], uint64_t m) {
-  switch (pat) {
-    case 0: sign_pat<R, NR, -1, 0, -1, 0>(a, m); return;
-    case 1: sign_pat<R, NR, 0, 0, -1, 0>(a, m); return;
-    case 2: sign_pat<R, NR, 0, 1, -1, 0>(a, m); return;
-    case 3: sign_pat<R, NR, 1, 0, -1, 0>(a, m); return;
-    case 4: sign_pat<R, NR, 1, 1, -1, 0>(a, m); return;
-    case 5: sign_pat<R, NR, 2, 0, -1, 0>(a, m); return;
-    case 6: sign_pat<R, NR, 2, 1, -1, 0>(a, m); return;
-    case 7: sign_pat<R, NR, 3, 0, -1, 0>(a, m); return;
-    case 8: sign_pat<R, NR, 3, 1, -1, 0>(a, m); return;
-    SK_SIGN_PAIR(0, 1, 0)
-    SK_SIGN_PAIR(0, 2, 1)
-    SK_SIGN_PAIR(0, 3, 2)
-    SK_SIGN_PAIR(1, 2, 3)
-    SK_SIGN_PAIR(1, 3, 4)
-    SK_SIGN_PAIR(2, 3, 5)
-    default: return;
-  }
-}
-#undef SK_SIGN_PAIR
-
-// Y on slot P (pairs with register slot Q == V; Q < 0: all pairs) when p:
-// y0 = -i a1 = (a1.y, -a1.x), y1 = i a0 = (-a0.y, a0.x) as masked swaps of
-// a0.x <-> a1.y and a0.y <-> a1.x plus two masked sign flips
-template <typename R, int NR, int P, int Q, int V>
-__device__ __forceinline__ void yswap_sel(vec2_t<R> (&a)[1 << NR], bool p) {
-  if constexpr (P < NR && (Q < 0 || (Q < NR && P != Q))) {
-    const uint64_t m = p ? ~0ull : 0ull, sb = p ? SignBit<R>::value : 0ull;
-#pragma unroll
-    for (int e = 0; e < (1 << NR); ++e) {
-      if (((e >> P) & 1) || (Q >= 0 && ((e >> Q) & 1) != V)) continue;
-      const int e1 = e | (1 << P);
-      R a0x = a[e].x, a0y = a[e].y, a1x = a[e1].x, a1y = a[e1].y;
-      swap_bits(a0x, a1y, m);
-      swap_bits(a0y, a1x, m);
-      a[e] = mk<R>(a0x, flip_bits(a0y, sb));
-      a[e1] = mk<R>(flip_bits(a1x, sb), a1y);
-    }
-  }
-}
 
 // real 2x2 on slot P: y0 = m00 a0 + m01 a1, y1 = m10 a0 + m11 a1 (2 paired
 // instructions per output in fp32, half the dense 2x2)
@@ -739,33 +662,80 @@ __device__ __forceinline__ void sel(int i, F&& f) {
   }
 }
 
-// phase / sign pattern codes (host pattern_of agrees): 0 = all elements;
-// 1 + 2P + VP = slot P == VP; 9 + 4 pair(P<Q) + 2VP + VQ = both conditions
-struct PatCode {
-  int p, vp, q, vq;
-};
-__host__ __device__ constexpr PatCode pat_code(int k) {
-  constexpr int pp[6] = {0, 0, 0, 1, 1, 2}, qq[6] = {1, 2, 3, 2, 3, 3};
-  return k == 0 ? PatCode{-1, 0, -1, 0}
-       : k <= 8 ? PatCode{(k - 1) / 2, (k - 1) % 2, -1, 0}
-                : PatCode{pp[(k - 9) / 4], ((k - 9) / 2) % 2, qq[(k - 9) / 4], (k - 9) % 2};
+// masked forms (one code path per slot instead of one per register-control
+// pattern: less hot code): the pairs / elements to touch are the bits of a
+// runtime mask em (already zero when the thread predicate fails)
+template <typename R, int NR, int P>
+__device__ __forceinline__ void swap_mask(vec2_t<R> (&a)[1 << NR], uint32_t em) {
+  if constexpr (P < NR) {
+#pragma unroll
+    for (int e = 0; e < (1 << NR); ++e) {
+      if ((e >> P) & 1) continue;
+      const uint64_t m = 0ull - (uint64_t)((em >> e) & 1u);
+      swap_bits(a[e].x, a[e | (1 << P)].x, m);
+      swap_bits(a[e].y, a[e | (1 << P)].y, m);
+    }
+  }
 }
 
-// LEAN dispatch: one uniform branch tree per op (opcode ranges, then the
-// slot / pattern index); thread predicates are selects, never exits
+template <typename R, int NR, int P>
+__device__ __forceinline__ void yswap_mask(vec2_t<R> (&a)[1 << NR], uint32_t em) {
+  if constexpr (P < NR) {
+#pragma unroll
+    for (int e = 0; e < (1 << NR); ++e) {
+      if ((e >> P) & 1) continue;
+      const int e1 = e | (1 << P);
+      const uint64_t m = 0ull - (uint64_t)((em >> e) & 1u), sb = m & SignBit<R>::value;
+      R a0x = a[e].x, a0y = a[e].y, a1x = a[e1].x, a1y = a[e1].y;
+      swap_bits(a0x, a1y, m);
+      swap_bits(a0y, a1x, m);
+      a[e] = mk<R>(a0x, flip_bits(a0y, sb));
+      a[e1] = mk<R>(flip_bits(a1x, sb), a1y);
+    }
+  }
+}
+
+template <typename R, int NR>
+__device__ __forceinline__ void sign_mask(vec2_t<R> (&a)[1 << NR], uint32_t em) {
+#pragma unroll
+  for (int e = 0; e < (1 << NR); ++e) {
+    const uint64_t sb = (0ull - (uint64_t)((em >> e) & 1u)) & SignBit<R>::value;
+    a[e] = mk<R>(flip_bits(a[e].x, sb), flip_bits(a[e].y, sb));
+  }
+}
+
+// LEAN dispatch: one uniform branch tree per op (opcode class, then the
+// slot); thread predicates are masks and selects, never exits
 template <typename R, int NR>
 __device__ __forceinline__ void lean_op(const LOp<R>& op, uint32_t opc, vec2_t<R> (&a)[1 << NR], uint64_t gthr) {
   const int o = (int)opc;
-  if (o < OPC_MATT) {  // unpredicated dense 2x2: most ops of a random circuit
-    vec2_t<R> c[8];
-    coefs_of<R>(op, c);
-    sel<0, 4>(o - OPC_MAT, [&](auto k) {
-      constexpr int P = decltype(k)::value;
-      if constexpr (P < NR) mat_full_c<R, NR, P>(a, c);
-    });
+  if (o < OPC_MATR) {
+    if (o < OPC_MATRP) {  // dense 2x2
+      vec2_t<R> c[8];
+      coefs_of<R>(op, c);
+      sel<0, 4>(o - OPC_MAT, [&](auto k) {
+        constexpr int P = decltype(k)::value;
+        if constexpr (P < NR) mat_full_c<R, NR, P>(a, c);
+      });
+    } else {  // real first column: m = c, s; mr = w, wr
+      const R c = op.m[0], sn = op.m[4];
+      const vec2_t<R> w = mk<R>(op.mr[0], op.mr[1]), wr = mk<R>(op.mr[2], op.mr[3]);
+      sel<0, 4>(o - OPC_MATRP, [&](auto k) { matrp_slot<R, NR, decltype(k)::value>(a, c, sn, w, wr); });
+    }
     return;
   }
-  if (o >= OPC_MATR && o < OPC_DIAG1) {  // real 2x2 (split 1q gates)
+  if (o >= OPC_SWAPM && o < OPC_DIAG1) {  // masked X / Y / sign couplers
+    const bool p = (gthr & op.tmask) == op.tval && (op.qmask == 0 || (gthr & op.qmask) != 0);
+    const uint32_t em = p ? op.h.emask : 0u;
+    if (o == OPC_SIGNM)
+      sign_mask<R, NR>(a, em);
+    else if (o >= OPC_YSWAPM)
+      sel<0, 4>(o - OPC_YSWAPM, [&](auto k) { yswap_mask<R, NR, decltype(k)::value>(a, em); });
+    else
+      sel<0, 4>(o - OPC_SWAPM, [&](auto k) { swap_mask<R, NR, decltype(k)::value>(a, em); });
+    return;
+  }
+  if (o < OPC_MATT) {  // real 2x2
     vec2_t<R> c[8];
     coefs_of<R>(op, c);
     sel<0, 4>(o - OPC_MATR, [&](auto k) {
@@ -774,22 +744,8 @@ __device__ __forceinline__ void lean_op(const LOp<R>& op, uint32_t opc, vec2_t<R
     });
     return;
   }
-  if (o >= OPC_MATRP) {  // real first column (split 1q gates): m = c, s; mr = w, wr
-    const R c = op.m[0], sn = op.m[4];
-    const vec2_t<R> w = mk<R>(op.mr[0], op.mr[1]), wr = mk<R>(op.mr[2], op.mr[3]);
-    sel<0, 4>(o - OPC_MATRP, [&](auto k) { matrp_slot<R, NR, decltype(k)::value>(a, c, sn, w, wr); });
-    return;
-  }
-  if (o >= OPC_DIAG1 && o < OPC_MATRP) {  // phase on one slot value
-    const vec2_t<R> c = mk<R>(op.m[0], op.m[1]);
-    sel<0, 8>(o - OPC_DIAG1, [&](auto k) {
-      constexpr int K = decltype(k)::value;
-      phase_slot<R, NR, K / 2, K % 2>(a, c);
-    });
-    return;
-  }
   const bool p = (gthr & op.tmask) == op.tval;
-  if (o < OPC_SWAPT) {  // OPC_MATT: dense 2x2 behind a thread predicate
+  if (o < OPC_MATQ) {  // dense 2x2 behind a thread predicate (identity where it fails)
     vec2_t<R> c[8];
     coefs_if<R>(op, c, p);
     sel<0, 4>(o - OPC_MATT, [&](auto k) {
@@ -798,11 +754,7 @@ __device__ __forceinline__ void lean_op(const LOp<R>& op, uint32_t opc, vec2_t<R
     });
     return;
   }
-  if (o < OPC_MATQ) {  // OPC_SWAPT: X on a slot
-    sel<0, 4>(o - OPC_SWAPT, [&](auto k) { swap_sel<R, NR, decltype(k)::value, -1, 0>(a, p); });
-    return;
-  }
-  if (o < OPC_SWAPQ) {  // OPC_MATQ: dense 2x2 on pairs with slot Q == V
+  if (o < OPC_SWAPM) {  // dense 2x2 on the pairs with slot Q == V
     vec2_t<R> c[8];
     coefs_if<R>(op, c, p);
     sel<0, 32>(o - OPC_MATQ, [&](auto k) {
@@ -811,40 +763,22 @@ __device__ __forceinline__ void lean_op(const LOp<R>& op, uint32_t opc, vec2_t<R
     });
     return;
   }
-  if (o < OPC_PHASE) {  // OPC_SWAPQ
-    sel<0, 32>(o - OPC_SWAPQ, [&](auto k) {
+  if (o < OPC_PHASE) {  // phase on one slot value
+    const vec2_t<R> c = mk<R>(op.m[0], op.m[1]);
+    sel<0, 8>(o - OPC_DIAG1, [&](auto k) {
       constexpr int K = decltype(k)::value;
-      swap_sel<R, NR, K / 8, (K / 2) % 4, K % 2>(a, p);
+      phase_slot<R, NR, K / 2, K % 2>(a, c);
     });
     return;
   }
-  if (o == OPC_PHASE) {  // general phase: selected multiplier per element
-    const vec2_t<R> c = (gthr & op.qmask) ? mk<R>(op.m[2], op.m[3]) : mk<R>(op.m[0], op.m[1]);
-    const uint32_t em = p ? op.h.emask : 0u;
+  // OPC_PHASE: a selected multiplier per element
+  const vec2_t<R> c = (gthr & op.qmask) ? mk<R>(op.m[2], op.m[3]) : mk<R>(op.m[0], op.m[1]);
+  const uint32_t em = p ? op.h.emask : 0u;
 #pragma unroll
-    for (int e = 0; e < (1 << NR); ++e) {
-      const bool hit = (em >> e) & 1u;
-      a[e] = PK<R>::mul(a[e], mk<R>(hit ? c.x : (R)1, hit ? c.y : (R)0));
-    }
-    return;
+  for (int e = 0; e < (1 << NR); ++e) {
+    const bool hit = (em >> e) & 1u;
+    a[e] = PK<R>::mul(a[e], mk<R>(hit ? c.x : (R)1, hit ? c.y : (R)0));
   }
-  if (o == OPC_SIGN) {  // by -1: sign-bit flips
-    const bool ps = p && (op.qmask == 0 || (gthr & op.qmask) != 0);
-    const uint64_t m = ps ? SignBit<R>::value : 0ull;
-    sel<0, 33>(op.h.pat, [&](auto k) {
-      constexpr PatCode pc = pat_code(decltype(k)::value);
-      sign_pat<R, NR, pc.p, pc.vp, pc.q, pc.vq>(a, m);
-    });
-    return;
-  }
-  if (o < OPC_YSWAPQ) {  // OPC_YSWAPT
-    sel<0, 4>(o - OPC_YSWAPT, [&](auto k) { yswap_sel<R, NR, decltype(k)::value, -1, 0>(a, p); });
-    return;
-  }
-  sel<0, 32>(o - OPC_YSWAPQ, [&](auto k) {  // OPC_YSWAPQ
-    constexpr int K = decltype(k)::value;
-    yswap_sel<R, NR, K / 8, (K / 2) % 4, K % 2>(a, p);
-  });
 }
 
 // Generic fused sweep (random circuits, mixed gate streams): NS compile-time
@@ -1510,7 +1444,7 @@ static uint32_t opcode_of(const HostKOp& k) {
   if (k.kind == K_PHASE && k.pat >= 0 && !(k.flags & ~(uint32_t)(F_TPRED | F_QMASK))) {
     // by -1 (CZ-type couplers): sign flips instead of complex multiplies
     const bool q = (k.flags & F_QMASK) != 0;
-    if (k.m[2] == -1 && k.m[3] == 0 && k.m[1] == 0 && k.m[0] == (q ? 1 : -1)) return OPC_SIGN;
+    if (k.m[2] == -1 && k.m[3] == 0 && k.m[1] == 0 && k.m[0] == (q ? 1 : -1)) return OPC_SIGNM;
     if (k.flags == 0 && k.pat >= 1 && k.pat <= 8) return OPC_DIAG1 + (k.pat - 1);  // one slot condition
     return OPC_PHASE;
   }
@@ -1531,12 +1465,11 @@ static uint32_t opcode_of(const HostKOp& k) {
   if (k.kind != K_MAT && !swap) return OPC_GENERIC;
   const bool tp = (k.flags & F_TPRED) != 0;
   const uint32_t full = slot_mask(k.nr, k.slot, 0);
-  if (k.emask == full)
-    return swap ? OPC_SWAPT + k.slot : ymat ? OPC_YSWAPT + k.slot : (tp ? OPC_MATT : OPC_MAT) + k.slot;
+  if ((swap || ymat) && (k.emask & ~full) == 0) return (swap ? OPC_SWAPM : OPC_YSWAPM) + k.slot;  // any register controls
+  if (k.emask == full) return (tp ? OPC_MATT : OPC_MAT) + k.slot;
   for (int q = 0; q < k.nr; ++q)  // one register-side control
     for (int v = 0; v < 2; ++v)
-      if (q != k.slot && k.emask == (full & slot_mask(k.nr, q, v)))
-        return (swap ? OPC_SWAPQ : ymat ? OPC_YSWAPQ : OPC_MATQ) + 2 * (4 * k.slot + q) + v;
+      if (q != k.slot && k.emask == (full & slot_mask(k.nr, q, v))) return OPC_MATQ + 2 * (4 * k.slot + q) + v;
   return OPC_GENERIC;
 }
 
@@ -1597,7 +1530,7 @@ static void lean_param(const DSweep& d, const std::vector<unsigned char>& buf, s
       x.m[j] = k[o].m[j];
       x.mr[j] = k[o].mr[j];
     }
-    if (x.h.opc >= OPC_MATRP && x.h.opc < OPC_END) {  // m = (c, s) at m[0], m[4]; mr = w, (-w.y, w.x)
+    if (x.h.opc >= OPC_MATRP && x.h.opc < OPC_MATRP + 4) {  // m = (c, s) at m[0], m[4]; mr = w, (-w.y, w.x)
       const double c = (double)k[o].m[0], sn = (double)k[o].m[4];
       double wx, wy;
       if (c >= sn) {
