@@ -301,6 +301,11 @@ inline const std::vector<std::pair<std::vector<long long>, CliffordEntry>>& clif
 
 // (word, phase) with m == phase * word-product within 1e-12, else false
 inline bool match_clifford_1q(const cd m[4], std::string* word, cd* phase) {
+  // quick reject (no allocation): a Clifford 2x2 up to phase has |m_ij|^2 in {0, 1/2, 1}
+  for (int i = 0; i < 4; ++i) {
+    const double a = std::norm(m[i]);
+    if (std::fabs(a) > 1e-9 && std::fabs(a - 0.5) > 1e-9 && std::fabs(a - 1.0) > 1e-9) return false;
+  }
   std::vector<long long> k;
   if (!canonical_key(m, &k)) return false;
   for (const auto& p : clifford_table()) {
