@@ -1515,9 +1515,13 @@ static void lean_param(const DSweep& d, const std::vector<unsigned char>& buf, s
   out.assign(sizeof(LSweep<R>), 0);
   LSweep<R>* ls = reinterpret_cast<LSweep<R>*>(out.data());
   ls->d = d;
+  static const int noops = [] {  // SK_SWEEP_NOOPS=1: data movement only (cost split, A/B timing)
+    const char* e = std::getenv("SK_SWEEP_NOOPS");
+    return e ? std::atoi(e) : 0;
+  }();
   for (int s = 0; s < d.nstages; ++s) {
     ls->d.st[s].op_begin -= first;
-    ls->d.st[s].op_end -= first;
+    ls->d.st[s].op_end = noops ? ls->d.st[s].op_begin : ls->d.st[s].op_end - first;
   }
   const KOp<R>* k = reinterpret_cast<const KOp<R>*>(buf.data());
   for (int o = first; o < last; ++o) {

@@ -22,7 +22,18 @@ timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
   --csv --log-file $out/pergate_c64.csv python scripts/pergate_bw.py 28 c64 > /dev/null 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
   --csv --log-file $out/pergate_c128.csv python scripts/pergate_bw.py 27 c128 > /dev/null 2>&1
+# one generic sweep of random 30x20 c64 (k_sweep LEAN)
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_sweep -s 4 -c 1 -o /tmp/ks -f \
+  python scripts/prof_rand.py 30 c64 > /dev/null 2>&1
+ncu -i /tmp/ks.ncu-rep --page raw --csv > $out/ks_raw.csv
+# sanitizers over the generic-sweep opcode tests
+for tool in memcheck racecheck; do
+  timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 --print-limit 20 \
+    python -m pytest -q -m gpu -p no:cacheprovider tests/test_sweep_opcodes_gpu.py -k couplers_only > $out/sanitize_sweep_$tool.log 2>&1
+  echo "$tool rc=$?" >> $out/sanitize_sweep.txt
+done
 # the other BASELINE configs and the engine
 timeout 1200 python scripts/bench_configs.py qft20 qft27 rand30 qft34 hybrid > $out/configs.jsonl 2>&1
 timeout 600 python scripts/engine_profile.py 5 > $out/engine.txt 2>&1
+timeout 600 python scripts/engine_phases.py >> $out/engine.txt 2>&1
 ls -la $out
