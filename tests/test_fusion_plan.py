@@ -111,3 +111,25 @@ def test_qft_five_register_bit_chunks():
     plan = fusion.plan_circuit(build_qft(27), dtype="c64", tile_bits=13, low_bits=4, qft_nreg=5)
     assert plan.nreg == 5 and [len(sp.stages) for sp in plan.sweeps] == [2, 2, 3]
     assert [op.nbits for st in plan.sweeps[0].stages for op in st.ops] == [4, 5]
+
+
+@pytest.mark.parametrize("seed", [3, 4])
+def test_split_1q_keeps_op_count_and_exactness(rng, seed):
+    """split_1q (phase carried to the next dense gate on the bit): same op
+    count, most dense gates in real-first-column form, and the ops applied in
+    order equal the unsplit ops to fp64 rounding on a random state."""
+    c = build_random_circuit(9, 10, seed)
+    ops, _ = fusion.lower(c)
+    ops = fusion.merge_1q(fusion.fuse_diagonal_runs(ops))
+    split = fusion.split_1q(ops)
+    assert len(split) == len(ops)
+    dense = [o for o in split if o.kind == fusion.MAT and not o.ctrl_mask]
+    realcol = [o for o in dense if o.m[1] == 0.0 and o.m[5] == 0.0 and o.m[0] >= 0 and o.m[4] >= 0]
+    assert len(realcol) >= len(dense) // 2
+    x = random_state(9, rng)
+    a, b = x.copy(), x.copy()
+    for o in ops:
+        fusion.apply_op_numpy(a, o)
+    for o in split:
+        fusion.apply_op_numpy(b, o)
+    assert np.max(np.abs(a - b)) < 1e-12
