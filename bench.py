@@ -229,18 +229,17 @@ class ClockSampler:
 # our arm
 # ---------------------------------------------------------------------------
 def _so_sha256() -> str | None:
-    import hashlib
+    """Device-code hash of the built library (the .nv_fatbin section; host
+    objects differ between identical builds)."""
+    from paper_2304_14969_b200 import _build
 
-    lib = ROOT / "paper_2304_14969_b200" / "libshardcu.so"
-    if not lib.exists():
-        return None
-    return hashlib.sha256(lib.read_bytes()).hexdigest()
+    return _build.device_code_sha256()
 
 
 def ncu_traffic(dtype: str, n: int):
     """DRAM bytes per launch of the dominant kernel from the committed ncu
     --set full summary, used ONLY when that capture was taken of this exact
-    libshardcu.so build (sha256 match) and workload; else None."""
+    libshardcu.so device code (sha256 of its .nv_fatbin) and workload; else None."""
     prof = ROOT / "profiles" / "ncu_summary.json"
     if not prof.exists():
         return None

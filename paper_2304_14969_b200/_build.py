@@ -23,6 +23,30 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", 
          "--expt-relaxed-constexpr", f"-I{INCLUDE}"]
 
 
+def device_code_sha256(lib: Path = LIB) -> str | None:
+    """sha256 of the .nv_fatbin section (the sm_100a device code) of the
+    library.  nvcc embeds temporary file names in host objects, so two builds
+    of the same sources differ as files; their device code does not."""
+    import hashlib
+    import struct
+
+    try:
+        b = lib.read_bytes()
+    except OSError:
+        return None
+    if b[:4] != b"\x7fELF" or b[4] != 2:  # 64-bit ELF only
+        return None
+    shoff, = struct.unpack_from("<Q", b, 0x28)
+    shentsize, shnum, shstrndx = struct.unpack_from("<HHH", b, 0x3A)
+    sec = [struct.unpack_from("<IIQQQQ", b, shoff + i * shentsize) for i in range(shnum)]
+    stroff = sec[shstrndx][4]
+    for name, _t, _f, _a, off, size in sec:
+        end = b.index(b"\0", stroff + name)
+        if b[stroff + name:end] == b".nv_fatbin":
+            return hashlib.sha256(b[off:off + size]).hexdigest()
+    return None
+
+
 def _nvcc() -> str:
     for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", "nvcc"):
         if cand and (os.path.sep not in cand or os.path.exists(cand)):

@@ -10,6 +10,11 @@ into profiles/:
 """
 import csv
 import hashlib
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+from paper_2304_14969_b200 import _build  # noqa: E402
 import io
 import json
 import sys
@@ -51,7 +56,8 @@ def summarise(path: Path):
 def main():
     tag = sys.argv[1]
     lib = ROOT / "paper_2304_14969_b200" / "libshardcu.so"
-    out = {"tag": tag, "so_sha256": hashlib.sha256(lib.read_bytes()).hexdigest(), "captures": {}}
+    out = {"tag": tag, "so_sha256": _build.device_code_sha256(lib), "so_sha256_of": ".nv_fatbin section",
+           "captures": {}}
     for arg in sys.argv[2:]:
         name, _, path = arg.partition("=")
         lines, per = summarise(Path(path))
