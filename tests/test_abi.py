@@ -40,3 +40,15 @@ def test_no_device_is_reported_not_faked():
 def test_struct_layouts_match_header():
     assert ctypes.sizeof(_lib.SkOp) == 4 * 4 + 8 * 2 + 8 * 8
     assert ctypes.sizeof(_lib.SkSweep) == 4 * (1 + 16 + 1 + 8 * 5 + 9 + 1)
+
+
+def test_device_code_hash_reads_the_fatbin(tmp_path):
+    """bench.py matches the committed ncu summary by the sha256 of the
+    library's .nv_fatbin section (identical device code across rebuilds)."""
+    from paper_2304_14969_b200 import _build
+
+    h = _build.device_code_sha256()
+    assert h is not None and len(h) == 64 and int(h, 16) >= 0
+    bogus = tmp_path / "not_elf.so"
+    bogus.write_bytes(b"not an elf file")
+    assert _build.device_code_sha256(bogus) is None

@@ -74,3 +74,25 @@ def test_couplers_only_vs_oracle(rng, dtype):
     prog.run(s)
     got = permute_qubits(s, prog.plan.order).amps
     assert np.max(np.abs(got - want)) < TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_sweep_beyond_param_table_vs_oracle(rng, dtype):
+    """A sweep with more ops than the LEAN parameter table holds (kLeanOps =
+    128) runs through the generic interpreter; same results."""
+    n = 8
+    r = np.random.default_rng(9)
+    gates = []
+    for _ in range(300):  # every gate on qubits 0..2: the ops pile into few stages of one sweep
+        a, b = (int(v) for v in r.choice(3, 2, replace=False))
+        gates.append(u3(*r.uniform(0, 2 * math.pi, 3), a) if r.random() < 0.5 else COUPLERS[int(r.integers(0, 6))](a, b))
+    c = Circuit(n, tuple(gates))
+    plan = fusion.plan_circuit(c, dtype=dtype, tile_bits=8, low_bits=2)
+    assert max(sum(len(st.ops) for st in sp.stages) for sp in plan.sweeps) > 128
+    x = random_state(n, rng)
+    want = O.dense_run(c.gates, x.copy(), gate_matrix)
+    prog = compile_circuit(c, dtype=dtype, tile_bits=8, low_bits=2)
+    s = DenseKet(n, x, dtype=dtype)
+    prog.run(s)
+    got = permute_qubits(s, prog.plan.order).amps
+    assert np.max(np.abs(got - want)) < TOL[dtype]
