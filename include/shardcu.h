@@ -195,7 +195,10 @@ typedef struct {
 
 /* Validate and upload a program for an n-qubit state of `dtype`.  Each
  * sweep's `nreg` is the register-bit count it was planned with
- * (sk_program_reg_bits gives the dtype default). */
+ * (sk_program_reg_bits gives the dtype default).  A sweep whose lowered ops
+ * all have fast paths and number at most 128 runs with its op table in the
+ * kernel's parameter space (k_sweep LEAN); longer or more general sweeps run
+ * through the op interpreter — same results, slower. */
 int sk_program_reg_bits(int dtype, int* nreg);
 int sk_program_create(int width, int dtype, int device, const sk_sweep* sweeps, int nsweeps,
                       const sk_op* ops, int nops, sk_program** out);
