@@ -705,9 +705,12 @@ __device__ __forceinline__ void sign_mask(vec2_t<R> (&a)[1 << NR], uint32_t em) 
 }
 
 // LEAN dispatch: one uniform branch tree per op (opcode class, then the
-// slot); thread predicates are masks and selects, never exits
-template <typename R, int NR>
-__device__ __forceinline__ void lean_op(const LOp<R>& op, uint32_t opc, vec2_t<R> (&a)[1 << NR], uint64_t gthr) {
+// slot); thread predicates are masks and selects, never exits.  H tiles per
+// thread (a[h], their index parts gthr[h]): one dispatch and one set of
+// (uniform) coefficients serve H independent element groups.
+template <typename R, int NR, int H>
+__device__ __forceinline__ void lean_op(const LOp<R>& op, uint32_t opc, vec2_t<R> (&a)[H][1 << NR],
+                                        const uint64_t (&gthr)[H]) {
   const int o = (int)opc;
   if (o < OPC_MATR) {
     if (o < OPC_MATRP) {  // dense 2x2
@@ -715,24 +718,41 @@ __device__ __forceinline__ void lean_op(const LOp<R>& op, uint32_t opc, vec2_t<R
       coefs_of<R>(op, c);
       sel<0, 4>(o - OPC_MAT, [&](auto k) {
         constexpr int P = decltype(k)::value;
-        if constexpr (P < NR) mat_full_c<R, NR, P>(a, c);
+#pragma unroll
+        for (int h = 0; h < H; ++h)
+          if constexpr (P < NR) mat_full_c<R, NR, P>(a[h], c);
       });
     } else {  // real first column: m = c, s; mr = w, wr
       const R c = op.m[0], sn = op.m[4];
       const vec2_t<R> w = mk<R>(op.mr[0], op.mr[1]), wr = mk<R>(op.mr[2], op.mr[3]);
-      sel<0, 4>(o - OPC_MATRP, [&](auto k) { matrp_slot<R, NR, decltype(k)::value>(a, c, sn, w, wr); });
+      sel<0, 4>(o - OPC_MATRP, [&](auto k) {
+#pragma unroll
+        for (int h = 0; h < H; ++h) matrp_slot<R, NR, decltype(k)::value>(a[h], c, sn, w, wr);
+      });
     }
     return;
   }
   if (o >= OPC_SWAPM && o < OPC_DIAG1) {  // masked X / Y / sign couplers
-    const bool p = (gthr & op.tmask) == op.tval && (op.qmask == 0 || (gthr & op.qmask) != 0);
-    const uint32_t em = p ? op.h.emask : 0u;
-    if (o == OPC_SIGNM)
-      sign_mask<R, NR>(a, em);
-    else if (o >= OPC_YSWAPM)
-      sel<0, 4>(o - OPC_YSWAPM, [&](auto k) { yswap_mask<R, NR, decltype(k)::value>(a, em); });
-    else
-      sel<0, 4>(o - OPC_SWAPM, [&](auto k) { swap_mask<R, NR, decltype(k)::value>(a, em); });
+    uint32_t em[H];
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      const bool p = (gthr[h] & op.tmask) == op.tval && (op.qmask == 0 || (gthr[h] & op.qmask) != 0);
+      em[h] = p ? op.h.emask : 0u;
+    }
+    if (o == OPC_SIGNM) {
+#pragma unroll
+      for (int h = 0; h < H; ++h) sign_mask<R, NR>(a[h], em[h]);
+    } else if (o >= OPC_YSWAPM) {
+      sel<0, 4>(o - OPC_YSWAPM, [&](auto k) {
+#pragma unroll
+        for (int h = 0; h < H; ++h) yswap_mask<R, NR, decltype(k)::value>(a[h], em[h]);
+      });
+    } else {
+      sel<0, 4>(o - OPC_SWAPM, [&](auto k) {
+#pragma unroll
+        for (int h = 0; h < H; ++h) swap_mask<R, NR, decltype(k)::value>(a[h], em[h]);
+      });
+    }
     return;
   }
   if (o < OPC_MATT) {  // real 2x2
@@ -740,44 +760,55 @@ __device__ __forceinline__ void lean_op(const LOp<R>& op, uint32_t opc, vec2_t<R
     coefs_of<R>(op, c);
     sel<0, 4>(o - OPC_MATR, [&](auto k) {
       constexpr int P = decltype(k)::value;
-      if constexpr (P < NR) matr_full_c<R, NR, P>(a, c);
+#pragma unroll
+      for (int h = 0; h < H; ++h)
+        if constexpr (P < NR) matr_full_c<R, NR, P>(a[h], c);
     });
     return;
   }
-  const bool p = (gthr & op.tmask) == op.tval;
   if (o < OPC_MATQ) {  // dense 2x2 behind a thread predicate (identity where it fails)
-    vec2_t<R> c[8];
-    coefs_if<R>(op, c, p);
-    sel<0, 4>(o - OPC_MATT, [&](auto k) {
-      constexpr int P = decltype(k)::value;
-      if constexpr (P < NR) mat_full_c<R, NR, P>(a, c);
-    });
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      vec2_t<R> c[8];
+      coefs_if<R>(op, c, (gthr[h] & op.tmask) == op.tval);
+      sel<0, 4>(o - OPC_MATT, [&](auto k) {
+        constexpr int P = decltype(k)::value;
+        if constexpr (P < NR) mat_full_c<R, NR, P>(a[h], c);
+      });
+    }
     return;
   }
   if (o < OPC_SWAPM) {  // dense 2x2 on the pairs with slot Q == V
-    vec2_t<R> c[8];
-    coefs_if<R>(op, c, p);
-    sel<0, 32>(o - OPC_MATQ, [&](auto k) {
-      constexpr int K = decltype(k)::value;
-      mat_q_c<R, NR, K / 8, (K / 2) % 4, K % 2>(a, c);
-    });
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      vec2_t<R> c[8];
+      coefs_if<R>(op, c, (gthr[h] & op.tmask) == op.tval);
+      sel<0, 32>(o - OPC_MATQ, [&](auto k) {
+        constexpr int K = decltype(k)::value;
+        mat_q_c<R, NR, K / 8, (K / 2) % 4, K % 2>(a[h], c);
+      });
+    }
     return;
   }
   if (o < OPC_PHASE) {  // phase on one slot value
     const vec2_t<R> c = mk<R>(op.m[0], op.m[1]);
     sel<0, 8>(o - OPC_DIAG1, [&](auto k) {
       constexpr int K = decltype(k)::value;
-      phase_slot<R, NR, K / 2, K % 2>(a, c);
+#pragma unroll
+      for (int h = 0; h < H; ++h) phase_slot<R, NR, K / 2, K % 2>(a[h], c);
     });
     return;
   }
   // OPC_PHASE: a selected multiplier per element
-  const vec2_t<R> c = (gthr & op.qmask) ? mk<R>(op.m[2], op.m[3]) : mk<R>(op.m[0], op.m[1]);
-  const uint32_t em = p ? op.h.emask : 0u;
 #pragma unroll
-  for (int e = 0; e < (1 << NR); ++e) {
-    const bool hit = (em >> e) & 1u;
-    a[e] = PK<R>::mul(a[e], mk<R>(hit ? c.x : (R)1, hit ? c.y : (R)0));
+  for (int h = 0; h < H; ++h) {
+    const vec2_t<R> c = (gthr[h] & op.qmask) ? mk<R>(op.m[2], op.m[3]) : mk<R>(op.m[0], op.m[1]);
+    const uint32_t em = (gthr[h] & op.tmask) == op.tval ? op.h.emask : 0u;
+#pragma unroll
+    for (int e = 0; e < (1 << NR); ++e) {
+      const bool hit = (em >> e) & 1u;
+      a[h][e] = PK<R>::mul(a[h][e], mk<R>(hit ? c.x : (R)1, hit ? c.y : (R)0));
+    }
   }
 }
 
@@ -792,73 +823,92 @@ __device__ __forceinline__ const DSweep& dsweep_of(const LSweep<R>& s) { return 
 template <typename R, bool LEAN>
 using SweepArg = std::conditional_t<LEAN, LSweep<R>, DSweep>;
 
-template <typename R, int NR, int NS, bool LEAN>
+// H = 2 (LEAN fp32): each CTA runs tiles 2b and 2b + 1 together, each thread
+// holding its 16 amplitudes of both, so every op dispatch and coefficient
+// load serves twice the arithmetic
+template <typename R, int NR, int NS, bool LEAN, int H = 1>
 __global__ void k_sweep(vec2_t<R>* __restrict__ amps, const __grid_constant__ SweepArg<R, LEAN> arg,
-                                                  const KOp<R>* __restrict__ ops, const uint4* __restrict__ thr) {
+                        const KOp<R>* __restrict__ ops, const uint4* __restrict__ thr) {
   using V = vec2_t<R>;
   const DSweep& sw = dsweep_of(arg);
   extern __shared__ __align__(16) unsigned char smraw[];
   constexpr int NE = 1 << NR;
   const uint32_t tid = threadIdx.x;
-  const uint64_t base = deposit(blockIdx.x, sw.brun, sw.nb);
   const int nthreads = blockDim.x;
+  const size_t tile_bytes = ((size_t)nthreads << NR) * sizeof(V);
+  uint64_t base[H];
+#pragma unroll
+  for (int h = 0; h < H; ++h) base[h] = deposit((uint64_t)blockIdx.x * H + h, sw.brun, sw.nb);
 
-  V a[NE];
+  V a[H][NE];
 #pragma unroll 1
   for (int s = 0; s < NS; ++s) {  // not unrolled: one copy of the op loop (its uniform index) per kernel
     const DStage& st = sw.st[s];
     const uint4 t = __ldg(thr + s * nthreads + tid);
-    const uint64_t gthr = base | ((uint64_t)t.y << 32 | t.x);
-    if (s == 0) {
-      const char* p = reinterpret_cast<const char*>(amps + gthr);
+    uint64_t gthr[H];
 #pragma unroll
-      for (int k = 0; k < NE; ++k) {
-        const int e = k ^ (k >> 1);
-        if (k) {
-          const int b = ctz_c(k);
-          p = ((e >> b) & 1) ? p + st.reg_goff[b] : p - st.reg_goff[b];
+    for (int h = 0; h < H; ++h) gthr[h] = base[h] | ((uint64_t)t.y << 32 | t.x);
+    if (s == 0) {
+#pragma unroll
+      for (int h = 0; h < H; ++h) {
+        const char* p = reinterpret_cast<const char*>(amps + gthr[h]);
+#pragma unroll
+        for (int k = 0; k < NE; ++k) {
+          const int e = k ^ (k >> 1);
+          if (k) {
+            const int b = ctz_c(k);
+            p = ((e >> b) & 1) ? p + st.reg_goff[b] : p - st.reg_goff[b];
+          }
+          a[h][e] = *reinterpret_cast<const V*>(p);
         }
-        a[e] = *reinterpret_cast<const V*>(p);
       }
     } else {
       __syncthreads();
-      uint32_t so = t.z;
 #pragma unroll
-      for (int k = 0; k < NE; ++k) {
-        const int e = k ^ (k >> 1);
-        if (k) so ^= st.reg_soff[ctz_c(k)];
-        a[e] = *reinterpret_cast<const V*>(smraw + so);
+      for (int h = 0; h < H; ++h) {
+        uint32_t so = t.z;
+#pragma unroll
+        for (int k = 0; k < NE; ++k) {
+          const int e = k ^ (k >> 1);
+          if (k) so ^= st.reg_soff[ctz_c(k)];
+          a[h][e] = *reinterpret_cast<const V*>(smraw + h * tile_bytes + so);
+        }
       }
     }
     if constexpr (LEAN) {  // every op of the sweep has a fast path: no interpreter in the loop
-      // warp reductions mark the op range warp-uniform (the stage loop is not
-      // unrolled, so nvcc would otherwise index the op table from vector
-      // registers): op fields then load with LDCU into uniform registers
-      for (int o = st.op_begin; o < st.op_end; ++o) lean_op<R, NR>(arg.op[o], arg.op[o].h.opc, a, gthr);
+      for (int o = st.op_begin; o < st.op_end; ++o) lean_op<R, NR, H>(arg.op[o], arg.op[o].h.opc, a, gthr);
     } else {
       // sweeps with ops outside the fast-path set are interpreted op by op
       // (inlining the fast-path table here too multiplied nvcc time)
-      for (int o = st.op_begin; o < st.op_end; ++o) apply_kop<R, NR>(ops + o, a, gthr);
+#pragma unroll
+      for (int h = 0; h < H; ++h)
+        for (int o = st.op_begin; o < st.op_end; ++o) apply_kop<R, NR>(ops + o, a[h], gthr[h]);
     }
     if (s == NS - 1) {
-      char* p = reinterpret_cast<char*>(amps + gthr);
 #pragma unroll
-      for (int k = 0; k < NE; ++k) {
-        const int e = k ^ (k >> 1);
-        if (k) {
-          const int b = ctz_c(k);
-          p = ((e >> b) & 1) ? p + st.reg_goff[b] : p - st.reg_goff[b];
+      for (int h = 0; h < H; ++h) {
+        char* p = reinterpret_cast<char*>(amps + gthr[h]);
+#pragma unroll
+        for (int k = 0; k < NE; ++k) {
+          const int e = k ^ (k >> 1);
+          if (k) {
+            const int b = ctz_c(k);
+            p = ((e >> b) & 1) ? p + st.reg_goff[b] : p - st.reg_goff[b];
+          }
+          *reinterpret_cast<V*>(p) = a[h][e];
         }
-        *reinterpret_cast<V*>(p) = a[e];
       }
     } else {
       if (s > 0) __syncthreads();
-      uint32_t so = t.z;
 #pragma unroll
-      for (int k = 0; k < NE; ++k) {
-        const int e = k ^ (k >> 1);
-        if (k) so ^= st.reg_soff[ctz_c(k)];
-        *reinterpret_cast<V*>(smraw + so) = a[e];
+      for (int h = 0; h < H; ++h) {
+        uint32_t so = t.z;
+#pragma unroll
+        for (int k = 0; k < NE; ++k) {
+          const int e = k ^ (k >> 1);
+          if (k) so ^= st.reg_soff[ctz_c(k)];
+          *reinterpret_cast<V*>(smraw + h * tile_bytes + so) = a[h][e];
+        }
       }
     }
   }
@@ -1728,6 +1778,11 @@ static int launch_one(sk_state* s, const sk_program* p, int i, DevCtx* c, int64_
       SK_ATTR((k_sweep<R, NR, 1, true>)); SK_ATTR((k_sweep<R, NR, 2, true>)); SK_ATTR((k_sweep<R, NR, 3, true>));
       SK_ATTR((k_sweep<R, NR, 4, true>)); SK_ATTR((k_sweep<R, NR, 5, true>)); SK_ATTR((k_sweep<R, NR, 6, true>));
       SK_ATTR((k_sweep<R, NR, 7, true>)); SK_ATTR((k_sweep<R, NR, 8, true>));
+      if constexpr (sizeof(R) == 4) {
+#define SK_ATTR2(NS_) SK_CUDA(cudaFuncSetAttribute(k_sweep<R, NR, NS_, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024));
+        SK_ATTR2(1) SK_ATTR2(2) SK_ATTR2(3) SK_ATTR2(4) SK_ATTR2(5) SK_ATTR2(6) SK_ATTR2(7) SK_ATTR2(8)
+#undef SK_ATTR2
+      }
     }
 #ifndef SK_DEV_SWEEP_ONLY
     SK_ATTR((k_qft<R, NR, 1>)); SK_ATTR((k_qft<R, NR, 2>)); SK_ATTR((k_qft<R, NR, 3>));
@@ -1775,6 +1830,12 @@ static int launch_one(sk_state* s, const sk_program* p, int i, DevCtx* c, int64_
     const KOp<R>* ops = (const KOp<R>*)p->d_ops;
     const uint4* thr = (const uint4*)p->d_thr + p->thr_off[i];
     const bool lean = !p->lean[i].empty() && use_lean_kernel();
+    // fp32 LEAN sweeps: two tiles per CTA (SK_SWEEP_H=1 runs one, A/B timing)
+    static const int hpair = [] {
+      const char* e = std::getenv("SK_SWEEP_H");
+      return e ? std::atoi(e) : 2;
+    }();
+    const bool two = lean && sizeof(R) == 4 && hpair == 2 && tiles >= 2 && tiles % 2 == 0;
     const LSweep<R>* ls = lean ? reinterpret_cast<const LSweep<R>*>(p->lean[i].data()) : nullptr;
     switch (d.nstages * 2 + (lean ? 1 : 0)) {
 #ifdef SK_DEV_SWEEP_ONLY
@@ -1785,7 +1846,13 @@ static int launch_one(sk_state* s, const sk_program* p, int i, DevCtx* c, int64_
 #endif
 #define SK_GS(NS_)                                                                                          \
   case 2 * NS_: SK_GENERIC_SWEEP(NS_)                                                                       \
-  case 2 * NS_ + 1: k_sweep<R, NR, NS_, true><<<(unsigned)tiles, threads, smem, c->stream>>>(d_amps, *ls, ops, thr); \
+  case 2 * NS_ + 1:                                                                                     \
+    if (two) {                                                                                           \
+      if constexpr (sizeof(R) == 4)                                                                      \
+        k_sweep<R, NR, NS_, true, 2><<<(unsigned)(tiles / 2), threads, 2 * smem, c->stream>>>(d_amps, *ls, ops, thr); \
+    } else {                                                                                             \
+      k_sweep<R, NR, NS_, true><<<(unsigned)tiles, threads, smem, c->stream>>>(d_amps, *ls, ops, thr);   \
+    }                                                                                                    \
     break;
       SK_GS(1) SK_GS(2) SK_GS(3) SK_GS(4) SK_GS(5) SK_GS(6) SK_GS(7) SK_GS(8)
 #undef SK_GS

@@ -40,7 +40,7 @@ MAX_STAGES = _lib.SK_MAX_STAGES
 
 # kernel geometry per dtype (csrc/sk_fused.cu): register bits, max tile bits,
 # low contiguous bits (256 B per warp access)
-GEOMETRY = {"c64": dict(nreg=4, tile=11, low=5, qft_tile=12, qft_low=4, qft_nreg=4),
+GEOMETRY = {"c64": dict(nreg=4, tile=11, low=4, qft_tile=12, qft_low=4, qft_nreg=4),
             "c128": dict(nreg=3, tile=10, low=4, qft_tile=11, qft_low=3, qft_nreg=4)}
 # Measured on B200 (scripts/tune_qft.py): QFT-27 c64 1.10 ms at T=12/low=4
 # (k_qft); c128 QFT windows use 4 register bits (16 amplitudes per thread):
@@ -50,7 +50,10 @@ GEOMETRY = {"c64": dict(nreg=4, tile=11, low=5, qft_tile=12, qft_low=4, qft_nreg
 # for 4-bit chunks at T=12 (half the occupancy costs more than the saved
 # exchange); random 30x20 c64 384 ms at T=11/low=5 vs 467 ms at T=13/low=5 and
 # c128 803 ms at T=10/low=4 vs 917 ms at T=12 (generic k_sweep: fewer, larger
-# tiles lose occupancy to its ~110 registers per thread).
+# tiles lose occupancy to its ~110 registers per thread).  Round 2 (LEAN op
+# tables in the parameter space, two tiles per CTA): random 30x20 c64
+# 192.6 ms at T=11/low=4 (30 sweeps) vs 199.9 ms at low=5 (34 sweeps),
+# 202.9 at T=10/low=4, 207.6 at T=12/low=4.
 
 
 @dataclass
