@@ -826,9 +826,9 @@ using SweepArg = std::conditional_t<LEAN, LSweep<R>, DSweep>;
 // H = 2 (LEAN fp32): each CTA runs tiles 2b and 2b + 1 together, each thread
 // holding its 16 amplitudes of both, so every op dispatch and coefficient
 // load serves twice the arithmetic
-template <typename R, int NR, int NS, bool LEAN, int H = 1>
-__global__ void k_sweep(vec2_t<R>* __restrict__ amps, const __grid_constant__ SweepArg<R, LEAN> arg,
-                        const KOp<R>* __restrict__ ops, const uint4* __restrict__ thr) {
+template <typename R, int NR, int NS, bool LEAN, int H>
+__device__ __forceinline__ void sweep_body(vec2_t<R>* __restrict__ amps, const SweepArg<R, LEAN>& arg,
+                                           const KOp<R>* __restrict__ ops, const uint4* __restrict__ thr) {
   using V = vec2_t<R>;
   const DSweep& sw = dsweep_of(arg);
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -912,6 +912,25 @@ __global__ void k_sweep(vec2_t<R>* __restrict__ amps, const __grid_constant__ Sw
       }
     }
   }
+}
+
+template <typename R, int NR, int NS, bool LEAN, int H = 1>
+__global__ void k_sweep(vec2_t<R>* __restrict__ amps, const __grid_constant__ SweepArg<R, LEAN> arg,
+                        const KOp<R>* __restrict__ ops, const uint4* __restrict__ thr) {
+  sweep_body<R, NR, NS, LEAN, H>(amps, arg, ops, thr);
+}
+
+#ifndef SK_SWEEP2_MINB
+#define SK_SWEEP2_MINB 4
+#endif
+// the two-tile fp32 kernel for 128-thread tiles (T = NR + 7), with a
+// register budget for SK_SWEEP2_MINB resident CTAs
+template <typename R, int NR, int NS>
+__global__ void __launch_bounds__(128, SK_SWEEP2_MINB) k_sweep2(vec2_t<R>* __restrict__ amps,
+                                                             const __grid_constant__ LSweep<R> arg,
+                                                             const KOp<R>* __restrict__ ops,
+                                                             const uint4* __restrict__ thr) {
+  sweep_body<R, NR, NS, true, 2>(amps, arg, ops, thr);
 }
 
 // ---------------------------------------------------------------------------
@@ -1779,7 +1798,7 @@ static int launch_one(sk_state* s, const sk_program* p, int i, DevCtx* c, int64_
       SK_ATTR((k_sweep<R, NR, 4, true>)); SK_ATTR((k_sweep<R, NR, 5, true>)); SK_ATTR((k_sweep<R, NR, 6, true>));
       SK_ATTR((k_sweep<R, NR, 7, true>)); SK_ATTR((k_sweep<R, NR, 8, true>));
       if constexpr (sizeof(R) == 4) {
-#define SK_ATTR2(NS_) SK_CUDA(cudaFuncSetAttribute(k_sweep<R, NR, NS_, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024));
+#define SK_ATTR2(NS_) SK_CUDA(cudaFuncSetAttribute(k_sweep2<R, NR, NS_>, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024));
         SK_ATTR2(1) SK_ATTR2(2) SK_ATTR2(3) SK_ATTR2(4) SK_ATTR2(5) SK_ATTR2(6) SK_ATTR2(7) SK_ATTR2(8)
 #undef SK_ATTR2
       }
@@ -1835,7 +1854,7 @@ static int launch_one(sk_state* s, const sk_program* p, int i, DevCtx* c, int64_
       const char* e = std::getenv("SK_SWEEP_H");
       return e ? std::atoi(e) : 2;
     }();
-    const bool two = lean && sizeof(R) == 4 && hpair == 2 && tiles >= 2 && tiles % 2 == 0;
+    const bool two = lean && sizeof(R) == 4 && hpair == 2 && tiles >= 2 && tiles % 2 == 0 && threads == 128;
     const LSweep<R>* ls = lean ? reinterpret_cast<const LSweep<R>*>(p->lean[i].data()) : nullptr;
     switch (d.nstages * 2 + (lean ? 1 : 0)) {
 #ifdef SK_DEV_SWEEP_ONLY
@@ -1849,7 +1868,7 @@ static int launch_one(sk_state* s, const sk_program* p, int i, DevCtx* c, int64_
   case 2 * NS_ + 1:                                                                                     \
     if (two) {                                                                                           \
       if constexpr (sizeof(R) == 4)                                                                      \
-        k_sweep<R, NR, NS_, true, 2><<<(unsigned)(tiles / 2), threads, 2 * smem, c->stream>>>(d_amps, *ls, ops, thr); \
+        k_sweep2<R, NR, NS_><<<(unsigned)(tiles / 2), threads, 2 * smem, c->stream>>>(d_amps, *ls, ops, thr); \
     } else {                                                                                             \
       k_sweep<R, NR, NS_, true><<<(unsigned)tiles, threads, smem, c->stream>>>(d_amps, *ls, ops, thr);   \
     }                                                                                                    \
