@@ -920,11 +920,28 @@ __global__ void k_sweep(vec2_t<R>* __restrict__ amps, const __grid_constant__ Sw
   sweep_body<R, NR, NS, LEAN, H>(amps, arg, ops, thr);
 }
 
+#ifndef SK_SWEEP1_MINB
+#define SK_SWEEP1_MINB 6
+#endif
+// one-tile LEAN kernel for 128-thread tiles with a register budget for
+// SK_SWEEP1_MINB resident CTAs (0: use k_sweep, no bound).  c128 random
+// 30x20: 472 ms at 6 (80 registers) vs 497 unbounded (96) and 511 at 7
+// (72 registers, spills); A/B alternated on one box.
+template <typename R, int NR, int NS>
+__global__ void __launch_bounds__(128, (SK_SWEEP1_MINB > 0 ? SK_SWEEP1_MINB : 1)) k_sweep1(vec2_t<R>* __restrict__ amps,
+                                                             const __grid_constant__ LSweep<R> arg,
+                                                             const KOp<R>* __restrict__ ops,
+                                                             const uint4* __restrict__ thr) {
+  sweep_body<R, NR, NS, true, 1>(amps, arg, ops, thr);
+}
+
 #ifndef SK_SWEEP2_MINB
 #define SK_SWEEP2_MINB 4
 #endif
 // the two-tile fp32 kernel for 128-thread tiles (T = NR + 7), with a
-// register budget for SK_SWEEP2_MINB resident CTAs
+// register budget for SK_SWEEP2_MINB resident CTAs.  c64 random 30x20:
+// 179.5 ms at 4 (128 registers) vs 192.4 unbounded (same register count:
+// the bound changes the schedule) and 210.7 at 5 (96 registers, spills).
 template <typename R, int NR, int NS>
 __global__ void __launch_bounds__(128, SK_SWEEP2_MINB) k_sweep2(vec2_t<R>* __restrict__ amps,
                                                              const __grid_constant__ LSweep<R> arg,
@@ -1869,6 +1886,8 @@ static int launch_one(sk_state* s, const sk_program* p, int i, DevCtx* c, int64_
     if (two) {                                                                                           \
       if constexpr (sizeof(R) == 4)                                                                      \
         k_sweep2<R, NR, NS_><<<(unsigned)(tiles / 2), threads, 2 * smem, c->stream>>>(d_amps, *ls, ops, thr); \
+    } else if (SK_SWEEP1_MINB > 0 && threads == 128) {                                                   \
+      k_sweep1<R, NR, NS_><<<(unsigned)tiles, threads, smem, c->stream>>>(d_amps, *ls, ops, thr);         \
     } else {                                                                                             \
       k_sweep<R, NR, NS_, true><<<(unsigned)tiles, threads, smem, c->stream>>>(d_amps, *ls, ops, thr);   \
     }                                                                                                    \
@@ -1887,9 +1906,14 @@ static int launch_sweeps(sk_state* s, const sk_program* p, int first, int count,
                          int64_t te = -1) {
   for (int i = first; i < first + count; ++i) {
     const int nr = p->sweeps[i].nr;
-#ifdef SK_DEV_SWEEP_ONLY  // fast development build: c64 generic LEAN sweeps only
-    if (s->dtype != SK_C64 || nr != 4) return set_error(SK_EVALUE, "development build: c64 4-bit sweeps only");
-    SK_TRY((launch_one<float, 4>(s, p, i, c, tb, te)));
+#ifdef SK_DEV_SWEEP_ONLY  // fast development build: generic LEAN sweeps only (c64 4-bit, c128 3-bit)
+    if (s->dtype == SK_C64 && nr == 4) {
+      SK_TRY((launch_one<float, 4>(s, p, i, c, tb, te)));
+    } else if (s->dtype == SK_C128 && nr == 3) {
+      SK_TRY((launch_one<double, 3>(s, p, i, c, tb, te)));
+    } else {
+      return set_error(SK_EVALUE, "development build: generic sweeps only");
+    }
     continue;
 #endif
     if (s->dtype == SK_C64 && nr == 5) {
