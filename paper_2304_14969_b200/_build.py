@@ -47,6 +47,36 @@ def device_code_sha256(lib: Path = LIB) -> str | None:
     return None
 
 
+def kernel_sass_sha256(pattern: str = "k_qft", lib: Path = LIB) -> str | None:
+    """sha256 of the SASS of the library's kernels whose name contains
+    `pattern` (cuobjdump, addresses stripped).  The key the committed ncu
+    summary is matched on: rebuilding identical sources has produced
+    different .nv_fatbin bytes but identical kernel code."""
+    import hashlib
+    import re
+    import shutil
+
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not Path(tool).exists() or not lib.exists():
+        return None
+    try:
+        out = subprocess.run([tool, "-sass", str(lib)], capture_output=True, text=True, timeout=120).stdout
+    except (OSError, subprocess.SubprocessError):
+        return None
+    h = hashlib.sha256()
+    keep = False
+    n = 0
+    for line in out.splitlines():
+        if "Function : " in line:
+            keep = pattern in line
+            n += keep
+        if keep:
+            line = re.sub(r"/\*[0-9a-fx]+\*/", "", line).strip()
+            if line:
+                h.update(line.encode() + b"\n")
+    return h.hexdigest() if n else None
+
+
 def _nvcc() -> str:
     for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", "nvcc"):
         if cand and (os.path.sep not in cand or os.path.exists(cand)):

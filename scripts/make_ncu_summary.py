@@ -56,8 +56,8 @@ def summarise(path: Path):
 def main():
     tag = sys.argv[1]
     lib = ROOT / "paper_2304_14969_b200" / "libshardcu.so"
-    out = {"tag": tag, "so_sha256": _build.device_code_sha256(lib), "so_sha256_of": ".nv_fatbin section",
-           "captures": {}}
+    out = {"tag": tag, "kqft_sass_sha256": _build.kernel_sass_sha256("k_qft", lib),
+           "so_sha256": _build.device_code_sha256(lib), "so_sha256_of": ".nv_fatbin section", "captures": {}}
     for arg in sys.argv[2:]:
         name, _, path = arg.partition("=")
         lines, per = summarise(Path(path))

@@ -52,3 +52,14 @@ def test_device_code_hash_reads_the_fatbin(tmp_path):
     bogus = tmp_path / "not_elf.so"
     bogus.write_bytes(b"not an elf file")
     assert _build.device_code_sha256(bogus) is None
+
+
+def test_kernel_sass_hash_is_stable_key():
+    """The ncu summary is matched on the SASS of the k_qft kernels."""
+    from paper_2304_14969_b200 import _build
+
+    h = _build.kernel_sass_sha256("k_qft")
+    if h is None:
+        pytest.skip("cuobjdump not available")
+    assert len(h) == 64 and h == _build.kernel_sass_sha256("k_qft")
+    assert _build.kernel_sass_sha256("no_such_kernel_name") is None
