@@ -6,6 +6,8 @@ import ctypes
 import re
 from pathlib import Path
 
+import pytest
+
 from paper_2304_14969_b200 import _lib
 
 HEADER = Path(__file__).resolve().parent.parent / "include" / "shardcu.h"
